@@ -1,0 +1,419 @@
+"""The two ConvBench algorithms as B200 drop-ins, plus the fused implicit-GEMM conv.
+
+Same entry points, signatures and phase nomenclature as the reference
+(pkg/src/convbench/algos.py); every step runs as a hand-written sm_100a kernel in
+libconvb200.so, called through the C ABI (include/convb200.h).  There is no CPU path:
+without the library or a GPU these functions raise.
+
+reference                                     here (kernel, phase)
+--------------------------------------------  ----------------------------------------------
+im2col_transform            algos.py:99-121   K1 cb_im2col_f32
+gemm                        algos.py:142-182  K3 split (IN_PACKING) + K4 cb_gemm (IN_MICROKERNEL)
+conv_baseline_im2col_gemm   algos.py:185-209  K1 (PRE_REORDER) -> K3 (IN_PACKING) ->
+                                              host tile plan (IN_TILING) ->
+                                              K4 cb_conv_gemm_cols + NCHW epilogue (IN_MICROKERNEL)
+conv_main_blocked_direct    algos.py:265-334  slice/chunk plan (PRE_ANALYSIS) -> K3 (PRE_REORDER)
+  ("SConv")                                   -> per L2-resident chunk of slices:
+                                                 tile plan (IN_TILING), K2 cb_sconv_pack_f32
+                                                 (IN_PACKING), K4 cb_sconv_gemm (IN_MICROKERNEL),
+                                                 K5 cb_unpack_f32 (IN_UNPACKING)
+conv_fused (new)                              K3 (PRE_REORDER) -> K6/K7 cb_conv_fused (IN_MICROKERNEL)
+
+Numerics: the tensor-core variants use a 3-product split (hi*hi + hi*lo + lo*hi) with fp32
+accumulation in TMEM; "ffma" is plain fp32.  All pass the path's parity gate
+max|y - y_ref| / sqrt(C/g*R*S) <= 1e-4 against the float64 reference.
+
+Inputs may be numpy arrays (uploaded before the first phase, result downloaded after the
+last, both outside the timed phases) or CUDA torch tensors (used in place; the result is
+a CUDA tensor).  Ledgers may be this package's PhaseLedger/EventLedger or the
+reference's PhaseLedger: with a host-clock ledger each device phase synchronises the
+stream before it closes so the host clock measures the kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from ._capi import UnsupportedDescriptorError
+from .descriptor import ConvDescriptor, output_shape
+from .timing import HOST_PHASES, Phase, PhaseLedger
+
+DEFAULT_VARIANT = "tc3xtf32"
+B200_L2_BYTES = 126 * 1024 * 1024
+
+__all__ = [
+    "CacheParams", "ConvInputs", "GemmBlocking", "UnsupportedDescriptorError",
+    "conv_baseline_im2col_gemm", "conv_fused", "conv_main_blocked_direct", "gemm",
+    "im2col_transform", "split_weights", "plan_tiles", "plan_sconv", "DEFAULT_VARIANT",
+]
+
+
+# ---------------------------------------------------------------------------------------
+# Boundary types (algos.py:35-84)
+# ---------------------------------------------------------------------------------------
+@dataclass
+class ConvInputs:
+    """Activation / weight / bias buffers tied to their descriptor (algos.py:39-59).
+
+    Buffers may be numpy arrays or torch tensors (CPU or CUDA)."""
+    desc: ConvDescriptor
+    input: object
+    weights: object
+    bias: object | None = None
+
+    def __post_init__(self) -> None:
+        d = self.desc
+        want_in = (d.batch, d.in_channels, d.in_h, d.in_w)
+        want_w = (d.out_channels, d.in_channels // d.groups, d.k_h, d.k_w)
+        if tuple(self.input.shape) != want_in:
+            raise ValueError(f"input shape {tuple(self.input.shape)}, descriptor wants {want_in}")
+        if tuple(self.weights.shape) != want_w:
+            raise ValueError(f"weights shape {tuple(self.weights.shape)}, descriptor wants {want_w}")
+        if d.has_bias:
+            if self.bias is None or tuple(self.bias.shape) != (d.out_channels,):
+                raise ValueError(f"descriptor has bias, need vector of length {d.out_channels}")
+        elif self.bias is not None:
+            raise ValueError("bias buffer given but descriptor has no bias")
+
+
+@dataclass(frozen=True)
+class GemmBlocking:
+    """CPU cache blocking of the reference GEMM (algos.py:62-77).  Accepted and validated
+    for signature compatibility; the GPU tile plan comes from cb_plan_tiles."""
+    mc: int = 128
+    kc: int = 256
+    nc: int = 512
+    mr: int = 8
+    nr: int = 8
+
+    def __post_init__(self) -> None:
+        if min(self.mc, self.kc, self.nc, self.mr, self.nr) < 1:
+            raise ValueError("blocking sizes must be >= 1")
+        if self.mc % self.mr:
+            raise ValueError(f"mc={self.mc} not a multiple of mr={self.mr}")
+        if self.nc % self.nr:
+            raise ValueError(f"nc={self.nc} not a multiple of nr={self.nr}")
+
+
+@dataclass(frozen=True)
+class CacheParams:
+    """Cache sizes the SConv planner fits slices into (algos.py:80-84).  On the GPU the
+    relevant cache is the 126 MB L2: one chunk of packed slices plus its accumulators is
+    kept within `l2_bytes // 2` so it never round-trips through HBM."""
+    l1_bytes: int = 228 * 1024
+    l2_bytes: int = B200_L2_BYTES
+
+
+# ---------------------------------------------------------------------------------------
+# device plumbing (torch: memory + streams only)
+# ---------------------------------------------------------------------------------------
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise _capi.ConvB200Error("no CUDA device: the B200 path has no CPU fallback")
+    return torch
+
+
+def _stream() -> int:
+    return _torch().cuda.current_stream().cuda_stream
+
+
+def _dev(a):
+    """(contiguous fp32 CUDA tensor, came_from_host)."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        host = not a.is_cuda
+        t = a.to(device="cuda", dtype=torch.float32).contiguous()
+        return t, host
+    arr = np.ascontiguousarray(a, dtype=np.float32)
+    return torch.from_numpy(arr).to("cuda"), True
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _host_result(t, host: bool, like=None):
+    if not host:
+        return t
+    out = t.cpu().numpy()
+    if like is not None and isinstance(like, np.ndarray) and like.dtype != np.float32:
+        out = out.astype(like.dtype)
+    return out
+
+
+class _phase:
+    """start/update around a region; device regions synchronise for host-clock ledgers.
+    The ledger is balanced even when the region raises (SURVEY.md 8(b) Errors)."""
+
+    __slots__ = ("ledger", "phase", "sync")
+
+    def __init__(self, ledger, phase: Phase):
+        self.ledger = ledger
+        self.phase = phase
+        self.sync = (not getattr(ledger, "device_timed", False)) and Phase(phase) not in HOST_PHASES
+
+    def __enter__(self):
+        self.ledger.start(self.phase)
+        return self
+
+    def __exit__(self, *exc):
+        if self.sync and exc[0] is None:
+            _torch().cuda.current_stream().synchronize()
+        self.ledger.update(self.phase)
+        return False
+
+
+def _cd(desc) -> _capi.CbConvDesc:
+    return _capi.cdesc(desc)
+
+
+# ---------------------------------------------------------------------------------------
+# K3: weight split
+# ---------------------------------------------------------------------------------------
+def split_weights(w2d, variant: str = DEFAULT_VARIANT):
+    """rows x kdim fp32 CUDA tensor -> (hi, lo) rows x split_kdim(kdim), zero padded.
+    tf32 halves are fp32 containers; bf16 halves are int16 bit patterns."""
+    torch = _torch()
+    if variant not in _capi.TC_VARIANTS:
+        raise ValueError(f"weight split is only defined for {_capi.TC_VARIANTS}")
+    lib = _capi.load()
+    rows, kdim = int(w2d.shape[0]), int(w2d.shape[1])
+    kp = _capi.split_kdim(kdim)
+    dt = torch.float32 if variant == "tc3xtf32" else torch.int16
+    hi = torch.empty((rows, kp), dtype=dt, device=w2d.device)
+    lo = torch.empty((rows, kp), dtype=dt, device=w2d.device)
+    _capi.check(lib.cb_weight_split(_capi.variant_id(variant), rows, kdim, w2d.data_ptr(),
+                                    hi.data_ptr(), lo.data_ptr(), _stream()))
+    return hi, lo
+
+
+def _pack_weights(w_dev, d, variant: str):
+    """Weights as the kernels consume them: (w_hi, w_lo, w_f32)."""
+    w2d = w_dev.reshape(d.out_channels, -1)
+    if variant in _capi.TC_VARIANTS:
+        hi, lo = split_weights(w2d, variant)
+        return hi, lo, None
+    return None, None, w2d.contiguous()
+
+
+def plan_tiles(desc, variant: str = DEFAULT_VARIANT, pixels: int = 0) -> dict:
+    """The tile plan (cb_plan_tiles) a conv launch over `pixels` pixels will use."""
+    lib = _capi.load()
+    tp = _capi.CbTilePlan()
+    _capi.check(lib.cb_plan_tiles(_capi.variant_id(variant), ctypes.byref(_cd(desc)), pixels,
+                                  ctypes.byref(tp)))
+    return tp.as_dict()
+
+
+# ---------------------------------------------------------------------------------------
+# K1 im2col_transform
+# ---------------------------------------------------------------------------------------
+def _im2col_dev(x_dev, d):
+    torch = _torch()
+    oh, ow = output_shape(d)
+    cols = torch.empty((d.in_channels * d.k_h * d.k_w, d.batch * oh * ow), dtype=torch.float32,
+                       device=x_dev.device)
+    _capi.check(_capi.load().cb_im2col_f32(ctypes.byref(_cd(d)), x_dev.data_ptr(),
+                                           cols.data_ptr(), _stream()))
+    return cols
+
+
+def im2col_transform(inputs) -> object:
+    """Bit-exact im2col matrix, rows (c, ky, kx), columns (n, oy, ox) (algos.py:99-121)."""
+    x, host = _dev(inputs.input)
+    return _host_result(_im2col_dev(x, inputs.desc), host, inputs.input)
+
+
+# ---------------------------------------------------------------------------------------
+# K4 gemm
+# ---------------------------------------------------------------------------------------
+def gemm(a, b, c_out, blocking: GemmBlocking, ledger, *, variant: str = DEFAULT_VARIANT) -> None:
+    """c_out = a @ b + c_out's initial contents (algos.py:142-182)."""
+    m, k = a.shape
+    kb, n = b.shape
+    if kb != k:
+        raise ValueError(f"inner dims disagree: {tuple(a.shape)} @ {tuple(b.shape)}")
+    if tuple(c_out.shape) != (m, n):
+        raise ValueError(f"c_out shape {tuple(c_out.shape)}, expected {(m, n)}")
+    torch = _torch()
+    lib = _capi.load()
+    a_d, _ = _dev(a)
+    b_d, _ = _dev(b)
+    c_is_dev = isinstance(c_out, torch.Tensor) and c_out.is_cuda and c_out.dtype == torch.float32 \
+        and c_out.is_contiguous()
+    c_d = c_out if c_is_dev else _dev(c_out)[0]
+    with _phase(ledger, Phase.IN_PACKING):
+        if variant in _capi.TC_VARIANTS:
+            a_hi, a_lo = split_weights(a_d, variant)
+            a_f32 = None
+        else:
+            a_hi = a_lo = None
+            a_f32 = a_d
+    with _phase(ledger, Phase.IN_TILING):
+        pass  # the GEMM tile plan is computed inside cb_gemm (host side, sub-microsecond)
+    with _phase(ledger, Phase.IN_MICROKERNEL):
+        _capi.check(lib.cb_gemm(_capi.variant_id(variant), m, n, k, _ptr(a_hi), _ptr(a_lo),
+                                _ptr(a_f32), b_d.data_ptr(), n, c_d.data_ptr(), n, 1, _stream()))
+    with _phase(ledger, Phase.IN_UNPACKING):
+        if not c_is_dev:
+            res = c_d.cpu()
+            if isinstance(c_out, np.ndarray):
+                c_out[...] = res.numpy()
+            else:
+                c_out.copy_(res)
+
+
+# ---------------------------------------------------------------------------------------
+# Im2col-GEMM baseline
+# ---------------------------------------------------------------------------------------
+def conv_baseline_im2col_gemm(inputs, ledger, blocking: GemmBlocking | None = None, *,
+                              variant: str = DEFAULT_VARIANT):
+    """Im2col + GEMM (algos.py:185-209): one explicit im2col (PRE_REORDER), weight
+    packing (IN_PACKING), tile planning (IN_TILING), then the tensor-core GEMM whose
+    epilogue writes NCHW + bias directly (IN_MICROKERNEL; no post reorder)."""
+    _ = blocking if blocking is not None else GemmBlocking()
+    torch = _torch()
+    lib = _capi.load()
+    d = inputs.desc
+    oh, ow = output_shape(d)
+    x, host = _dev(inputs.input)
+    w, _ = _dev(inputs.weights)
+    b = _dev(inputs.bias)[0] if inputs.bias is not None else None
+    y = torch.empty((d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
+    cd = _cd(d)
+    with _phase(ledger, Phase.PRE_REORDER):
+        cols = _im2col_dev(x, d)
+    with _phase(ledger, Phase.IN_PACKING):
+        w_hi, w_lo, w_f32 = _pack_weights(w, d, variant)
+    with _phase(ledger, Phase.IN_TILING):
+        tp = _capi.CbTilePlan()
+        _capi.check(lib.cb_plan_tiles(_capi.variant_id(variant), ctypes.byref(cd), 0,
+                                      ctypes.byref(tp)))
+    with _phase(ledger, Phase.IN_MICROKERNEL):
+        _capi.check(lib.cb_conv_gemm_cols(_capi.variant_id(variant), ctypes.byref(cd),
+                                          cols.data_ptr(), _ptr(w_hi), _ptr(w_lo), _ptr(w_f32),
+                                          _ptr(b), y.data_ptr(), _stream()))
+    return _host_result(y, host, inputs.input)
+
+
+# ---------------------------------------------------------------------------------------
+# SConv (blocked direct)
+# ---------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SConvPlan:
+    band_rows: int
+    num_slices: int
+    chunks: tuple[tuple[int, int, int, int], ...]   # (first_slice, count, pix_begin, pix_count)
+    max_chunk_pixels: int
+
+
+def plan_sconv(desc, cache: CacheParams | None = None) -> SConvPlan:
+    """GPU slice plan (the role of _plan_tiles, algos.py:254-262): slices are bands of
+    output rows; consecutive slices are grouped into chunks whose packed slices plus
+    accumulators fit in half the L2, so pack -> microkernel -> unpack of a chunk stays
+    on chip."""
+    cache = cache if cache is not None else CacheParams()
+    lib = _capi.load()
+    d = desc
+    oh, ow = output_shape(d)
+    kdim = d.in_channels * d.k_h * d.k_w
+    per_pixel = 4 * (kdim + d.out_channels)
+    budget = max(per_pixel * ow, cache.l2_bytes // 2)
+    max_slice_px = max(ow, min(oh * ow, budget // per_pixel))
+    cd = _cd(d)
+    sp = _capi.CbSlicePlan()
+    _capi.check(lib.cb_sconv_plan(ctypes.byref(cd), max_slice_px, ctypes.byref(sp)))
+    slice_px = sp.band_rows * ow
+    per_chunk = max(1, budget // (per_pixel * slice_px))
+    chunks = []
+    jb, jc = ctypes.c_int64(), ctypes.c_int64()
+    for first in range(0, sp.num_slices, per_chunk):
+        cnt = min(per_chunk, sp.num_slices - first)
+        _capi.check(lib.cb_sconv_range(ctypes.byref(cd), ctypes.byref(sp), first, cnt,
+                                       ctypes.byref(jb), ctypes.byref(jc)))
+        chunks.append((first, cnt, jb.value, jc.value))
+    return SConvPlan(sp.band_rows, sp.num_slices, tuple(chunks), max(c[3] for c in chunks))
+
+
+def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *,
+                             variant: str = DEFAULT_VARIANT):
+    """Sliced convolution (algos.py:265-334) on the GPU.
+
+    PRE_ANALYSIS plans slices and L2-sized chunks once; PRE_REORDER packs the weights;
+    then per chunk: IN_TILING (tile plan of the chunk), IN_PACKING (K2 packs the chunk's
+    slices from the unpadded input, boundary taps zero), IN_MICROKERNEL (K4 on the
+    slices), IN_UNPACKING (K5 adds the chunk's accumulators + bias into NCHW)."""
+    d = inputs.desc
+    if d.groups != 1 or d.dil_h != 1 or d.dil_w != 1:
+        raise UnsupportedDescriptorError(
+            f"blocked direct requires groups == 1 and dilation == 1, "
+            f"got groups={d.groups}, dilation=({d.dil_h}, {d.dil_w})")
+    torch = _torch()
+    lib = _capi.load()
+    oh, ow = output_shape(d)
+    x, host = _dev(inputs.input)
+    w, _ = _dev(inputs.weights)
+    b = _dev(inputs.bias)[0] if inputs.bias is not None else None
+    y = torch.empty((d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
+    cd = _cd(d)
+    vid = _capi.variant_id(variant)
+
+    with _phase(ledger, Phase.PRE_ANALYSIS):
+        plan = plan_sconv(d, cache)
+        sp = _capi.CbSlicePlan(plan.band_rows, plan.num_slices)
+    with _phase(ledger, Phase.PRE_REORDER):
+        w_hi, w_lo, w_f32 = _pack_weights(w, d, variant)
+    kdim = d.in_channels * d.k_h * d.k_w
+    slices = torch.empty(kdim * plan.max_chunk_pixels, dtype=torch.float32, device=x.device)
+    acc = torch.empty(d.out_channels * plan.max_chunk_pixels, dtype=torch.float32,
+                      device=x.device)
+    st = _stream()
+    tp = _capi.CbTilePlan()
+    for first, cnt, _jb, jc in plan.chunks:
+        with _phase(ledger, Phase.IN_TILING):
+            _capi.check(lib.cb_plan_tiles(vid, ctypes.byref(cd), jc, ctypes.byref(tp)))
+        with _phase(ledger, Phase.IN_PACKING):
+            _capi.check(lib.cb_sconv_pack_f32(ctypes.byref(cd), ctypes.byref(sp), first, cnt,
+                                              x.data_ptr(), slices.data_ptr(), st))
+        with _phase(ledger, Phase.IN_MICROKERNEL):
+            _capi.check(lib.cb_sconv_gemm(vid, ctypes.byref(cd), ctypes.byref(sp), first, cnt,
+                                          slices.data_ptr(), _ptr(w_hi), _ptr(w_lo), _ptr(w_f32),
+                                          acc.data_ptr(), st))
+        with _phase(ledger, Phase.IN_UNPACKING):
+            _capi.check(lib.cb_unpack_f32(ctypes.byref(cd), ctypes.byref(sp), first, cnt,
+                                          acc.data_ptr(), _ptr(b), y.data_ptr(), st))
+    return _host_result(y, host, inputs.input)
+
+
+# ---------------------------------------------------------------------------------------
+# Fused implicit-GEMM convolution (K6 / K7)
+# ---------------------------------------------------------------------------------------
+def conv_fused(inputs, ledger=None, *, variant: str = DEFAULT_VARIANT, packed=None):
+    """y = conv(x, w) + b in one kernel from NCHW (no im2col workspace).
+
+    PRE_REORDER: weight split (skipped when `packed` = (w_hi, w_lo, w_f32) is given);
+    IN_MICROKERNEL: the fused kernel (gather producers build the split activation tiles
+    in shared memory; tcgen05 MMAs accumulate in TMEM; NCHW epilogue with bias)."""
+    ledger = ledger if ledger is not None else PhaseLedger()
+    torch = _torch()
+    lib = _capi.load()
+    d = inputs.desc
+    oh, ow = output_shape(d)
+    x, host = _dev(inputs.input)
+    b = _dev(inputs.bias)[0] if inputs.bias is not None else None
+    y = torch.empty((d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
+    if packed is None:
+        w, _ = _dev(inputs.weights)
+        with _phase(ledger, Phase.PRE_REORDER):
+            packed = _pack_weights(w, d, variant)
+    w_hi, w_lo, w_f32 = packed
+    with _phase(ledger, Phase.IN_MICROKERNEL):
+        _capi.check(lib.cb_conv_fused(_capi.variant_id(variant), ctypes.byref(_cd(d)),
+                                      x.data_ptr(), _ptr(w_hi), _ptr(w_lo), _ptr(w_f32), _ptr(b),
+                                      y.data_ptr(), _stream()))
+    return _host_result(y, host, inputs.input)

@@ -1,0 +1,149 @@
+// cb_common.cuh -- shared host/device helpers for libconvb200 (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "convb200.h"
+
+namespace cb {
+
+// ------------------------------------------------------------------------------------
+// Error reporting (thread-local; returned through cb_last_error_string()).
+// ------------------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+
+// ------------------------------------------------------------------------------------
+// Conv geometry, resolved once on the host and passed by value to kernels.
+// Mirrors output_shape (descriptor.py:84-92): floor semantics.
+// ------------------------------------------------------------------------------------
+struct Geom {
+    int N, C, H, W, K, R, S;
+    int sh, sw, ph, pw, dh, dw, G;
+    int P, Q;        // output spatial dims
+    int cpg, kpg;    // channels / output channels per group
+    int kdim;        // cpg * R * S  (GEMM reduction length per group)
+    int kdim_pad;    // cb_split_kdim(kdim)
+    int PQ, HW, RS;
+    int64_t npix;    // N * P * Q
+};
+
+int make_geom(const cb_conv_desc* d, Geom* g);  // CB_OK or CB_ERR_INVALID
+
+inline int32_t round_up(int32_t a, int32_t b) { return (a + b - 1) / b * b; }
+inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int sm_count();  // cached multiProcessorCount of the current device
+
+// ------------------------------------------------------------------------------------
+// Pixel addressing modes shared by the GEMM/conv kernels.
+//
+// Every kernel walks "pixels" j in [0, npix) (the GEMM column / TMEM lane dimension)
+// and "reduction" k in [0, kdim).  Source (activation-side) operands are either
+// gathered from NCHW (implicit im2col) or linear in k per pixel:
+//     addr(j, k) = base(j) + k * kstride(j)
+// which covers the im2col matrix (base=j, kstride=ld) and the SConv slice buffer
+// (base = kdim*j0 + (j-j0), kstride = slice pixels).  Outputs are always linear:
+//     out(j, f) = obase(j) + f * okstride(j)
+// covering NCHW (obase = n*K*PQ + p, okstride = PQ), a plain row-major matrix and the
+// per-slice accumulator buffer.
+// ------------------------------------------------------------------------------------
+enum SrcMode : int { SRC_CONV = 0, SRC_MATRIX = 1, SRC_SLICES = 2 };
+enum DstMode : int { DST_NCHW = 0, DST_MATRIX = 1, DST_SLICES = 2 };
+
+struct PixMap {
+    int src_mode, dst_mode;
+    int64_t src_ld;      // SRC_MATRIX row stride (group g starts at row g*kdim)
+    int64_t dst_ld;      // DST_MATRIX row stride
+    int band_rows;       // SLICES: output rows per slice
+    int64_t j_begin;     // first pixel of this launch; slice buffers start at this pixel
+    int64_t j_count;     // pixels processed by this launch
+};
+
+__device__ __forceinline__ void slice_of(const Geom& g, int band_rows, int64_t j, int64_t& j0,
+                                         int& np) {
+    int64_t n = j / g.PQ;
+    int p = (int)(j - n * g.PQ);
+    int oy = p / g.Q;
+    int y0 = (oy / band_rows) * band_rows;
+    int rows = min(band_rows, g.P - y0);
+    np = rows * g.Q;
+    j0 = n * g.PQ + (int64_t)y0 * g.Q;
+}
+
+// Linear source address components for pixel j (SRC_MATRIX / SRC_SLICES).
+__device__ __forceinline__ void src_linear(const Geom& g, const PixMap& pm, int64_t j,
+                                           int64_t& base, int64_t& kstride) {
+    if (pm.src_mode == SRC_MATRIX) {
+        base = j;
+        kstride = pm.src_ld;
+    } else {
+        int64_t j0;
+        int np;
+        slice_of(g, pm.band_rows, j, j0, np);
+        base = (int64_t)g.kdim * (j0 - pm.j_begin) + (j - j0);
+        kstride = np;
+    }
+}
+
+// Output address components for pixel j.
+__device__ __forceinline__ void dst_linear(const Geom& g, const PixMap& pm, int64_t j,
+                                           int64_t& base, int64_t& okstride) {
+    if (pm.dst_mode == DST_NCHW) {
+        int64_t n = j / g.PQ;
+        int64_t p = j - n * g.PQ;
+        base = n * (int64_t)g.K * g.PQ + p;
+        okstride = g.PQ;
+    } else if (pm.dst_mode == DST_MATRIX) {
+        base = j;
+        okstride = pm.dst_ld;
+    } else {
+        int64_t j0;
+        int np;
+        slice_of(g, pm.band_rows, j, j0, np);
+        base = (int64_t)g.K * (j0 - pm.j_begin) + (j - j0);
+        okstride = np;
+    }
+}
+
+// first pixel of slice s (slices of one image are consecutive bands of band_rows rows)
+inline int64_t slice_pixel_begin(const Geom& g, int band_rows, int64_t s) {
+    const int64_t per_img = (g.P + band_rows - 1) / band_rows;
+    const int64_t n = s / per_img, b = s - n * per_img;
+    if (n >= g.N) return g.npix;
+    return n * g.PQ + b * band_rows * (int64_t)g.Q;
+}
+
+// ------------------------------------------------------------------------------------
+// Precision splits.  tf32: 1 sign, 8 exponent, 10 mantissa bits, stored in an fp32
+// container with the low 13 bits zero.  cvt.rna = round to nearest, ties away.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+struct Split2 {
+    float hi, lo;
+};
+__device__ __forceinline__ Split2 split_tf32(float x) {
+    float hi = tf32_rna(x);
+    float lo = tf32_rna(x - hi);
+    return {hi, lo};
+}
+
+// bf16 round-to-nearest-even of an fp32 value, returned as raw bits.
+__device__ __forceinline__ uint16_t bf16_rn_bits(float x) {
+    uint16_t r;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
+    return __uint_as_float(((uint32_t)b) << 16);
+}
+
+}  // namespace cb

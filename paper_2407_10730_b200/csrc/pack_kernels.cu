@@ -1,0 +1,217 @@
+// pack_kernels.cu -- the HBM-bound packing kernels of the two stepwise algorithms.
+//
+//   K1 im2col_kernel<false>  im2col_transform        (algos.py:99-121)   -> PRE_REORDER
+//   K2 im2col_kernel<true>   SConv per-slice packing (algos.py:305-324)  -> IN_PACKING
+//   K3 weight_split_kernel   wmat / _pack_a_panels   (algos.py:124-130, :202, :291)
+//   K5 unpack_kernel         out[...] += acc         (algos.py:331-333)  -> IN_UNPACKING
+//   fill_bias_kernel         _alloc_output           (algos.py:87-96)
+//
+// K1/K2 are pure copies (bit-exact with the reference): each thread owns VEC
+// consecutive output columns (pixels) of one packed row (c, ky, kx), so stores are
+// coalesced 16-byte vectors and the loads of a warp walk one input row.  The input is
+// read through L2 once from HBM (every tap re-reads it from L2); the packed matrix is
+// written once: algorithmic bytes = 4 * (N*C*H*W + C*R*S*N*P*Q).
+#include "cb_common.cuh"
+
+namespace cb {
+
+constexpr int PACK_VEC = 4;
+constexpr int PACK_THREADS = 256;
+
+template <bool SLICED>
+__global__ void __launch_bounds__(PACK_THREADS)
+im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ out, int band_rows,
+              int64_t j_begin, int64_t j_count, int64_t col_blocks, bool vec_ok) {
+    const int64_t bid = blockIdx.x;
+    const int row = (int)(bid / col_blocks);
+    const int64_t cblk = bid - (int64_t)row * col_blocks;
+    const int64_t jl = (cblk * PACK_THREADS + threadIdx.x) * PACK_VEC;
+    if (jl >= j_count) return;
+    const int64_t j = j_begin + jl;
+
+    // row = (c, ky, kx) over ALL input channels (groups are contiguous row blocks)
+    const int c = row / g.RS;
+    const int rs = row - c * g.RS;
+    const int ky = rs / g.S;
+    const int kx = rs - ky * g.S;
+
+    int64_t n = j / g.PQ;
+    int p = (int)(j - n * g.PQ);
+    int oy = p / g.Q;
+    int ox = p - oy * g.Q;
+
+    float v[PACK_VEC];
+#pragma unroll
+    for (int i = 0; i < PACK_VEC; ++i) {
+        float val = 0.f;
+        if (jl + i < j_count) {
+            const int iy = oy * g.sh - g.ph + ky * g.dh;
+            const int ix = ox * g.sw - g.pw + kx * g.dw;
+            if ((unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W)
+                val = __ldg(x + (((int64_t)n * g.C + c) * g.H + iy) * g.W + ix);
+        }
+        v[i] = val;
+        if (++ox == g.Q) {
+            ox = 0;
+            if (++oy == g.P) {
+                oy = 0;
+                ++n;
+            }
+        }
+    }
+
+    if (!SLICED) {
+        float* dst = out + (int64_t)row * j_count + jl;
+        if (vec_ok) {
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < PACK_VEC; ++i)
+                if (jl + i < j_count) dst[i] = v[i];
+        }
+    } else {
+        // slice buffer: the slice holding pixels [j0, j0+np) starts at
+        // out + kdim*(j0 - j_begin), laid out (k, pixel)
+        if (vec_ok) {
+            int64_t j0;
+            int np;
+            slice_of(g, band_rows, j, j0, np);
+            float* dst = out + (int64_t)g.kdim * (j0 - j_begin) + (int64_t)row * np + (j - j0);
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < PACK_VEC; ++i) {
+                if (jl + i < j_count) {
+                    int64_t j0;
+                    int np;
+                    slice_of(g, band_rows, j + i, j0, np);
+                    out[(int64_t)g.kdim * (j0 - j_begin) + (int64_t)row * np + (j + i - j0)] =
+                        v[i];
+                }
+            }
+        }
+    }
+}
+
+// K3: rows x kdim (row-major) -> hi/lo rows x kdim_pad, zero padded.
+template <bool BF16>
+__global__ void weight_split_kernel(int rows, int kdim, int kdim_pad, const float* __restrict__ w,
+                                    void* __restrict__ hi_out, void* __restrict__ lo_out) {
+    const int64_t total = (int64_t)rows * kdim_pad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / kdim_pad);
+        const int k = (int)(i - (int64_t)r * kdim_pad);
+        const float v = k < kdim ? w[(int64_t)r * kdim + k] : 0.f;
+        if (BF16) {
+            const uint16_t h = bf16_rn_bits(v);
+            const uint16_t l = bf16_rn_bits(v - bf16_bits_to_f32(h));
+            static_cast<uint16_t*>(hi_out)[i] = h;
+            static_cast<uint16_t*>(lo_out)[i] = l;
+        } else {
+            const Split2 s = split_tf32(v);
+            static_cast<float*>(hi_out)[i] = s.hi;
+            static_cast<float*>(lo_out)[i] = s.lo;
+        }
+    }
+}
+
+// K5: y[n, f, p] = bias[f] + acc[slice(j)][f][j - j0] for the pixels [j_begin, +j_count)
+__global__ void unpack_kernel(Geom g, int band_rows, int64_t j_begin, int64_t j_count,
+                              const float* __restrict__ acc, const float* __restrict__ bias,
+                              float* __restrict__ y) {
+    const int64_t total = j_count * g.K;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(i / j_count);
+        const int64_t j = j_begin + (i - (int64_t)f * j_count);
+        const int64_t n = j / g.PQ;
+        const int64_t p = j - n * g.PQ;
+        int64_t j0;
+        int np;
+        slice_of(g, band_rows, j, j0, np);
+        const float b = bias ? __ldg(bias + f) : 0.f;
+        y[(n * g.K + f) * g.PQ + p] =
+            b + __ldg(acc + (int64_t)g.K * (j0 - j_begin) + (int64_t)f * np + (j - j0));
+    }
+}
+
+// y (N, K, P*Q) = bias broadcast (or 0): the output initialisation of _alloc_output.
+__global__ void fill_bias_kernel(int64_t images, int K, int PQ, const float* __restrict__ bias,
+                                 float* __restrict__ y) {
+    const int64_t total = images * K * PQ;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)((i / PQ) % K);
+        y[i] = bias ? __ldg(bias + f) : 0.f;
+    }
+}
+
+static int grid_for(int64_t total, int threads) {
+    const int64_t want = ceil_div64(total, threads);
+    const int64_t cap = (int64_t)sm_count() * 16;
+    return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+int launch_im2col(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
+                  int64_t j_begin, int64_t j_count, cudaStream_t st) {
+    if (j_count == 0) return CB_OK;
+    const int64_t col_blocks = ceil_div64(j_count, (int64_t)PACK_THREADS * PACK_VEC);
+    const int64_t rows = (int64_t)g.C * g.RS;
+    const int64_t blocks = rows * col_blocks;
+    if (blocks > 0x7fffffffLL) return fail(CB_ERR_UNSUPPORTED, "im2col grid too large");
+    const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    if (!sliced) {
+        const bool vec_ok = aligned && (j_count % PACK_VEC == 0);
+        im2col_kernel<false><<<(unsigned)blocks, PACK_THREADS, 0, st>>>(
+            g, x, out, band_rows, j_begin, j_count, col_blocks, vec_ok);
+    } else {
+        // a VEC group never straddles a slice when slice starts are multiples of VEC
+        const bool vec_ok = aligned && (g.Q % PACK_VEC == 0) && (j_begin % PACK_VEC == 0) &&
+                            (j_count % PACK_VEC == 0);
+        im2col_kernel<true><<<(unsigned)blocks, PACK_THREADS, 0, st>>>(
+            g, x, out, band_rows, j_begin, j_count, col_blocks, vec_ok);
+    }
+    return check_launch(sliced ? "sconv_pack" : "im2col");
+}
+
+int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float* w, void* hi,
+                        void* lo, cudaStream_t st) {
+    const int64_t total = (int64_t)rows * kdim_pad;
+    if (total == 0) return CB_OK;
+    const int grid = grid_for(total, 256);
+    if (bf16)
+        weight_split_kernel<true><<<grid, 256, 0, st>>>(rows, kdim, kdim_pad, w, hi, lo);
+    else
+        weight_split_kernel<false><<<grid, 256, 0, st>>>(rows, kdim, kdim_pad, w, hi, lo);
+    return check_launch("weight_split");
+}
+
+int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count,
+                  const float* acc, const float* bias, float* y, cudaStream_t st) {
+    const int64_t total = j_count * g.K;
+    if (total == 0) return CB_OK;
+    unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>(g, band_rows, j_begin, j_count, acc,
+                                                         bias, y);
+    return check_launch("unpack");
+}
+
+int launch_fill_bias(int64_t images, int K, int PQ, const float* bias, float* y, cudaStream_t st) {
+    const int64_t total = images * K * PQ;
+    if (total == 0) return CB_OK;
+    fill_bias_kernel<<<grid_for(total, 256), 256, 0, st>>>(images, K, PQ, bias, y);
+    return check_launch("fill_bias");
+}
+
+int pre_init_output(const Geom& g, const PixMap& pm, int zero_kind, const float* bias, float* out,
+                    cudaStream_t st) {
+    if (zero_kind == 1) return launch_fill_bias(g.N, g.K, g.PQ, bias, out, st);
+    if (zero_kind == 2) {
+        cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)g.K * pm.j_count, st);
+        if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
+        return CB_OK;
+    }
+    return fail(CB_ERR_INVALID, "output cannot be pre-initialised for split-K");
+}
+
+}  // namespace cb

@@ -1,0 +1,159 @@
+"""GPU parity: every kernel of the path against the CPU oracle on identical seeded inputs.
+
+Gate (BASELINE.json north_star): max|y - y_ref| / sqrt(C/g*R*S) <= 1e-4 for
+convolutions (written below as TOL); packing kernels are bit-exact.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from corpus import cfg, corpus
+from oracle import conv_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+VARIANTS = ["tc3xtf32", "tc3xbf16", "ffma"]
+
+
+def _inputs(d, seed=0):
+    from paper_2407_10730_b200.algos import ConvInputs
+    x, w, b = orc.make_inputs(d, seed)
+    return ConvInputs(desc=d, input=x, weights=w, bias=b), (x, w, b)
+
+
+def _check_conv(d, got, ref, tol=TOL):
+    assert got.shape == ref.shape and got.dtype == np.float32
+    err = orc.normalized_max_err(got, ref, orc.reduction_len(d))
+    assert err <= tol, f"{d}: normalized max err {err:.3e} > {tol:g}"
+    return err
+
+
+SMALL = corpus(24, seed=7, spatial=(9, 14)) + corpus(6, seed=8, spatial=(5, 9), batch=(2, 3))
+SUPPORTED = corpus(12, seed=31, spatial=(8, 14), supported_only=True) + \
+    corpus(4, seed=32, spatial=(6, 10), supported_only=True, batch=(2, 3))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_fused_matches_oracle_on_corpus(cuda, variant):
+    from paper_2407_10730_b200.algos import conv_fused
+    for d in SMALL:
+        inp, (x, w, b) = _inputs(d)
+        _check_conv(d, conv_fused(inp, variant=variant), orc.conv_direct_naive(d, x, w, b))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_im2col_gemm_matches_oracle_on_corpus(cuda, variant):
+    from paper_2407_10730_b200.algos import conv_baseline_im2col_gemm
+    from paper_2407_10730_b200.timing import PhaseLedger
+    for d in SMALL:
+        inp, (x, w, b) = _inputs(d)
+        got = conv_baseline_im2col_gemm(inp, PhaseLedger(), variant=variant)
+        _check_conv(d, got, orc.conv_direct_naive(d, x, w, b))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_sconv_matches_oracle_on_supported(cuda, variant):
+    from paper_2407_10730_b200.algos import CacheParams, conv_main_blocked_direct
+    from paper_2407_10730_b200.timing import PhaseLedger
+    for i, d in enumerate(SUPPORTED):
+        inp, (x, w, b) = _inputs(d)
+        # alternate default plan and a tiny budget that forces many slices / chunks
+        cache = None if i % 2 == 0 else CacheParams(l2_bytes=8 * 1024)
+        got = conv_main_blocked_direct(inp, PhaseLedger(), cache=cache, variant=variant)
+        _check_conv(d, got, orc.conv_direct_naive(d, x, w, b))
+
+
+def test_im2col_bit_exact(cuda):
+    from paper_2407_10730_b200.algos import im2col_transform
+    for d in SMALL + [cfg("cfg1"), cfg("cfg2a"), cfg("cfg2b"), cfg("cfg3", batch=2)]:
+        inp, (x, _, _) = _inputs(d)
+        got = im2col_transform(inp)
+        want = orc.im2col(d, x)
+        assert got.shape == want.shape
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), d
+
+
+def test_slice_pack_bit_exact(cuda):
+    import torch
+    from paper_2407_10730_b200 import _capi
+    import ctypes
+    lib = _capi.load()
+    for d in SUPPORTED[:8] + [cfg("cfg3", batch=2)]:
+        _, (x, _, _) = _inputs(d)
+        oh, ow = orc.output_shape(d)
+        for band in (1, 3, oh):
+            cd = _capi.cdesc(d)
+            sp = _capi.CbSlicePlan()
+            _capi.check(lib.cb_sconv_plan(ctypes.byref(cd), band * ow, ctypes.byref(sp)))
+            assert sp.band_rows == min(band, oh)
+            first, count = sp.num_slices // 3, max(1, sp.num_slices - sp.num_slices // 3 - 1)
+            want = orc.slice_pack(d, x, sp.band_rows, first, count)
+            xd = torch.from_numpy(x).cuda()
+            out = torch.full((want.size + 64,), float("nan"), device="cuda")
+            _capi.check(lib.cb_sconv_pack_f32(ctypes.byref(cd), ctypes.byref(sp), first, count,
+                                              xd.data_ptr(), out.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream))
+            got = out.cpu().numpy()
+            assert np.array_equal(got[:want.size].view(np.uint32), want.view(np.uint32)), (d, band)
+            assert np.isnan(got[want.size:]).all(), "pack wrote past its slice range"
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_gemm_dropin(cuda, variant):
+    from paper_2407_10730_b200.algos import GemmBlocking, gemm
+    from paper_2407_10730_b200.timing import PhaseLedger
+    rng = np.random.default_rng(1)
+    for m, k, n in [(17, 13, 19), (1, 1, 1), (64, 300, 257), (300, 77, 1000)]:
+        a = (rng.random((m, k), dtype=np.float32) * 2 - 1)
+        b = (rng.random((k, n), dtype=np.float32) * 2 - 1)
+        c = (rng.random((m, n), dtype=np.float32) * 2 - 1)
+        want = a.astype(np.float64) @ b.astype(np.float64) + c
+        gemm(a, b, c, GemmBlocking(), PhaseLedger(), variant=variant)
+        err = float(np.abs(c - want).max()) / np.sqrt(k)
+        assert err <= TOL, (m, k, n, err)
+    # reference known answers (test_algos.py:95-125)
+    a = np.array([[3.0]], np.float32)
+    c = np.zeros((1, 1), np.float32)
+    gemm(a, np.array([[-2.0]], np.float32), c, GemmBlocking(), PhaseLedger(), variant=variant)
+    assert c[0, 0] == -6.0
+    c = np.full((2, 2), 10.0, np.float32)
+    gemm(np.ones((2, 2), np.float32), np.ones((2, 2), np.float32), c, GemmBlocking(),
+         PhaseLedger(), variant=variant)
+    assert (c == 12.0).all()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2a", "cfg2b", "cfg3", "cfg4"])
+def test_baseline_configs_all_paths(cuda, name):
+    """The five BASELINE.json configurations at full size through all three algorithms."""
+    from paper_2407_10730_b200.algos import (conv_baseline_im2col_gemm, conv_fused,
+                                             conv_main_blocked_direct)
+    from paper_2407_10730_b200.timing import PhaseLedger
+    d = cfg(name)
+    inp, (x, w, b) = _inputs(d)
+    ref = orc.conv_im2col64(d, x, w, b)
+    errs = {}
+    for variant in ("tc3xtf32", "tc3xbf16"):
+        errs[("fused", variant)] = _check_conv(d, conv_fused(inp, variant=variant), ref)
+    errs[("fused", "ffma")] = _check_conv(d, conv_fused(inp, variant="ffma"), ref)
+    errs["im2col"] = _check_conv(d, conv_baseline_im2col_gemm(inp, PhaseLedger()), ref)
+    errs["sconv"] = _check_conv(d, conv_main_blocked_direct(inp, PhaseLedger()), ref)
+    print(name, {str(k): f"{v:.2e}" for k, v in errs.items()})
+
+
+def test_known_answers(cuda):
+    """All-ones 3x3 with bias 0.5 -> 9.5 everywhere (reference test_algos.py:193-200)."""
+    from paper_2407_10730_b200.algos import (ConvInputs, conv_baseline_im2col_gemm, conv_fused,
+                                             conv_main_blocked_direct)
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    from paper_2407_10730_b200.timing import PhaseLedger
+    d = ConvDescriptor(batch=1, in_channels=1, in_h=5, in_w=5, out_channels=1, k_h=3, k_w=3,
+                       has_bias=True)
+    inp = ConvInputs(desc=d, input=np.ones((1, 1, 5, 5), np.float32),
+                     weights=np.ones((1, 1, 3, 3), np.float32), bias=np.full(1, 0.5, np.float32))
+    for fn in (conv_baseline_im2col_gemm, conv_main_blocked_direct):
+        assert (fn(inp, PhaseLedger()) == 9.5).all()
+    for v in VARIANTS:
+        assert (conv_fused(inp, variant=v) == 9.5).all()
