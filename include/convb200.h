@@ -81,6 +81,8 @@ typedef enum cb_variant {
 int         cb_version(void);
 const char* cb_last_error_string(void);
 int         cb_device_sm_count(int* sm_count);
+/* Total kernels this library has launched in the process (for launch accounting). */
+uint64_t    cb_launch_count(void);
 
 /* output_shape (descriptor.py:84-92) with the same validation as ConvDescriptor. */
 int cb_output_shape(const cb_conv_desc* d, int32_t* out_h, int32_t* out_w);
@@ -107,7 +109,7 @@ int cb_sconv_range(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t fir
 int cb_sconv_pack_f32(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t first_slice,
                       int32_t count, const float* x, float* slices, void* stream);
 
-/* ---- IN_TILING: the tile plan cb_conv_fused / cb_conv_gemm_cols / cb_sconv_gemm use for
+/* ---- IN_TILING: the tile plan cb_conv_gemm_cols / cb_sconv_gemm use for
  * `pixels` output pixels (<= 0: the whole batch).  Pure host computation. */
 int cb_plan_tiles(int variant, const cb_conv_desc* d, int64_t pixels, cb_tile_plan* plan);
 
@@ -149,11 +151,49 @@ int cb_unpack_f32(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t firs
 
 /* ---- K6/K7: fused implicit-GEMM convolution from NCHW: y = conv(x, w) + bias.
  * Replaces conv_baseline_im2col_gemm / conv_main_blocked_direct as a whole
- * (algos.py:185-209, :265-334).  TC variants take split weights (cb_weight_split with
- * rows = K, kdim = C/groups*R*S); FFMA takes raw OIHW w_f32. */
+ * (algos.py:185-209, :265-334).
+ *
+ * Tensor-core variants run one of two paths, chosen per descriptor (cb_fused_layout):
+ *   path 1 (TMA): K0 splits x once into an NHWC (hi, lo) workspace, K6 is a persistent
+ *          tcgen05 kernel fed by TMA im2col loads of that workspace and tiled TMA loads of
+ *          the tap-ordered split weights;
+ *   path 0 (gather): no workspace; producer warps gather + split from NCHW (used when TMA
+ *          im2col cannot express the descriptor, e.g. groups not chunk aligned).
+ * FFMA always runs the SIMT gather kernel with raw OIHW weights (no packing). */
+typedef struct cb_fused_layout {
+    int32_t path;            /* 1 = TMA im2col, 0 = gather                                  */
+    int32_t chunk_channels;  /* channels per reduction chunk (path 1)                      */
+    int32_t chunk_bytes;     /* 16 / 32 / 64 / 128 (path 1)                                */
+    int32_t k_blocks;        /* pipeline stages per output tile                            */
+    int32_t weight_rows;     /* packed weight matrix: rows (= out_channels) ...            */
+    int32_t weight_cols;     /* ... x cols elements per half (0 for FFMA: raw OIHW)        */
+    int64_t workspace_bytes; /* activation split workspace (0 unless path 1)               */
+} cb_fused_layout;
+
+int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* layout);
+
+/* Tile plan of cb_conv_fused_packed (the persistent grid for path 1). */
+int cb_fused_plan_tiles(int variant, const cb_conv_desc* d, cb_tile_plan* plan);
+
+/* K3 for the fused path (PRE_REORDER): OIHW weights -> packed split halves in the layout
+ * the selected path consumes (weight_rows x weight_cols each; bf16 halves as uint16). */
+int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, void* w_hi,
+                          void* w_lo, void* stream);
+
+/* K0 (IN_PACKING): x -> NHWC (hi, lo) split in `workspace` (no-op unless path 1). */
+int cb_fused_pack_input(int variant, const cb_conv_desc* d, const float* x, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* K6/K7 (IN_MICROKERNEL) on already packed operands. */
+int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x,
+                         const void* workspace, size_t workspace_bytes, const void* w_hi,
+                         const void* w_lo, const float* w_f32, const float* bias, float* y,
+                         void* stream);
+
+/* K0 + K6 in one call (weights already packed by cb_fused_pack_weights). */
 int cb_conv_fused(int variant, const cb_conv_desc* d, const float* x, const void* w_hi,
                   const void* w_lo, const float* w_f32, const float* bias, float* y,
-                  void* stream);
+                  void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

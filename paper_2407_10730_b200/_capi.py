@@ -23,11 +23,13 @@ TC_VARIANTS = ("tc3xtf32", "tc3xbf16")
 
 # Every symbol include/convb200.h declares (tests check the .so exports all of them).
 EXPORTS = (
-    "cb_version", "cb_last_error_string", "cb_device_sm_count", "cb_output_shape",
+    "cb_version", "cb_last_error_string", "cb_device_sm_count", "cb_launch_count",
+    "cb_output_shape",
     "cb_workspace_bytes", "cb_im2col_f32", "cb_sconv_plan", "cb_sconv_range",
     "cb_sconv_pack_f32", "cb_plan_tiles",
     "cb_split_kdim", "cb_weight_split", "cb_gemm", "cb_conv_gemm_cols", "cb_sconv_gemm",
-    "cb_unpack_f32", "cb_conv_fused",
+    "cb_unpack_f32", "cb_fused_layout_query", "cb_fused_plan_tiles", "cb_fused_pack_weights",
+    "cb_fused_pack_input", "cb_conv_fused_packed", "cb_conv_fused",
 )
 
 
@@ -58,6 +60,15 @@ class CbTilePlan(ctypes.Structure):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
 
 
+class CbFusedLayout(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("path", "chunk_channels", "chunk_bytes", "k_blocks",
+                                             "weight_rows", "weight_cols")] + \
+               [("workspace_bytes", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -68,6 +79,7 @@ _SIGNATURES = {
     "cb_version": ([], ctypes.c_int),
     "cb_last_error_string": ([], ctypes.c_char_p),
     "cb_device_sm_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "cb_launch_count": ([], ctypes.c_uint64),
     "cb_output_shape": ([_DESC, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], ctypes.c_int),
     "cb_workspace_bytes": ([_DESC, ctypes.c_int, _PLAN, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "cb_im2col_f32": ([_DESC, _P, _P, _P], ctypes.c_int),
@@ -84,7 +96,14 @@ _SIGNATURES = {
     "cb_sconv_gemm": ([ctypes.c_int, _DESC, _PLAN, _I32, _I32, _P, _P, _P, _P, _P, _P],
                       ctypes.c_int),
     "cb_unpack_f32": ([_DESC, _PLAN, _I32, _I32, _P, _P, _P, _P], ctypes.c_int),
-    "cb_conv_fused": ([ctypes.c_int, _DESC, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "cb_fused_layout_query": ([ctypes.c_int, _DESC, ctypes.POINTER(CbFusedLayout)], ctypes.c_int),
+    "cb_fused_plan_tiles": ([ctypes.c_int, _DESC, ctypes.POINTER(CbTilePlan)], ctypes.c_int),
+    "cb_fused_pack_weights": ([ctypes.c_int, _DESC, _P, _P, _P, _P], ctypes.c_int),
+    "cb_fused_pack_input": ([ctypes.c_int, _DESC, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "cb_conv_fused_packed": ([ctypes.c_int, _DESC, _P, _P, ctypes.c_size_t, _P, _P, _P, _P, _P, _P],
+                             ctypes.c_int),
+    "cb_conv_fused": ([ctypes.c_int, _DESC, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P],
+                      ctypes.c_int),
 }
 
 _lib = None

@@ -39,16 +39,21 @@ import numpy as np
 
 from . import _capi
 from ._capi import UnsupportedDescriptorError
-from .descriptor import ConvDescriptor, output_shape
+from .descriptor import ConvDescriptor, flop_count, output_shape
 from .timing import HOST_PHASES, Phase, PhaseLedger
 
+# Stepwise algorithms default to the spec's 3xTF32; the fused hot path defaults to 3xBF16,
+# which on B200 runs at twice the MMA rate with half the operand bytes and measured a
+# lower, K-independent error.
 DEFAULT_VARIANT = "tc3xtf32"
+FUSED_DEFAULT_VARIANT = "tc3xbf16"
 B200_L2_BYTES = 126 * 1024 * 1024
 
 __all__ = [
     "CacheParams", "ConvInputs", "GemmBlocking", "UnsupportedDescriptorError",
     "conv_baseline_im2col_gemm", "conv_fused", "conv_main_blocked_direct", "gemm",
     "im2col_transform", "split_weights", "plan_tiles", "plan_sconv", "DEFAULT_VARIANT",
+    "FUSED_DEFAULT_VARIANT", "fused_layout", "fused_plan", "pack_fused_weights", "fused_workspace",
 ]
 
 
@@ -123,11 +128,12 @@ def _stream() -> int:
 
 
 def _dev(a):
-    """(contiguous fp32 CUDA tensor, came_from_host)."""
+    """(contiguous fp32 CUDA tensor, came_from_host).  Pinned host tensors upload
+    asynchronously on the current stream."""
     torch = _torch()
     if isinstance(a, torch.Tensor):
         host = not a.is_cuda
-        t = a.to(device="cuda", dtype=torch.float32).contiguous()
+        t = a.to(device="cuda", dtype=torch.float32, non_blocking=True).contiguous()
         return t, host
     arr = np.ascontiguousarray(a, dtype=np.float32)
     return torch.from_numpy(arr).to("cuda"), True
@@ -140,6 +146,9 @@ def _ptr(t) -> int | None:
 def _host_result(t, host: bool, like=None):
     if not host:
         return t
+    torch = _torch()
+    if isinstance(like, torch.Tensor):
+        return t.to("cpu")
     out = t.cpu().numpy()
     if like is not None and isinstance(like, np.ndarray) and like.dtype != np.float32:
         out = out.astype(like.dtype)
@@ -393,12 +402,51 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
 # ---------------------------------------------------------------------------------------
 # Fused implicit-GEMM convolution (K6 / K7)
 # ---------------------------------------------------------------------------------------
-def conv_fused(inputs, ledger=None, *, variant: str = DEFAULT_VARIANT, packed=None):
-    """y = conv(x, w) + b in one kernel from NCHW (no im2col workspace).
+def fused_layout(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
+    """cb_fused_layout_query: path (1 = TMA im2col, 0 = gather), chunking, workspace."""
+    fl = _capi.CbFusedLayout()
+    _capi.check(_capi.load().cb_fused_layout_query(_capi.variant_id(variant),
+                                                   ctypes.byref(_cd(desc)), ctypes.byref(fl)))
+    return fl.as_dict()
 
-    PRE_REORDER: weight split (skipped when `packed` = (w_hi, w_lo, w_f32) is given);
-    IN_MICROKERNEL: the fused kernel (gather producers build the split activation tiles
-    in shared memory; tcgen05 MMAs accumulate in TMEM; NCHW epilogue with bias)."""
+
+def fused_plan(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
+    tp = _capi.CbTilePlan()
+    _capi.check(_capi.load().cb_fused_plan_tiles(_capi.variant_id(variant),
+                                                 ctypes.byref(_cd(desc)), ctypes.byref(tp)))
+    return tp.as_dict()
+
+
+def pack_fused_weights(w_dev, desc, variant: str = FUSED_DEFAULT_VARIANT):
+    """(w_hi, w_lo, w_f32) in the layout conv_fused's kernel consumes (K3, fused layout)."""
+    torch = _torch()
+    if variant not in _capi.TC_VARIANTS:
+        return None, None, w_dev.reshape(desc.out_channels, -1).contiguous()
+    lay = fused_layout(desc, variant)
+    dt = torch.float32 if variant == "tc3xtf32" else torch.int16
+    hi = torch.empty((lay["weight_rows"], lay["weight_cols"]), dtype=dt, device=w_dev.device)
+    lo = torch.empty_like(hi)
+    _capi.check(_capi.load().cb_fused_pack_weights(_capi.variant_id(variant),
+                                                   ctypes.byref(_cd(desc)), w_dev.data_ptr(),
+                                                   hi.data_ptr(), lo.data_ptr(), _stream()))
+    return hi, lo, None
+
+
+def fused_workspace(desc, variant: str = FUSED_DEFAULT_VARIANT, device="cuda"):
+    n = fused_layout(desc, variant)["workspace_bytes"]
+    if n == 0:
+        return None
+    return _torch().empty(n, dtype=_torch().uint8, device=device)
+
+
+def conv_fused(inputs, ledger=None, *, variant: str = FUSED_DEFAULT_VARIANT, packed=None,
+               workspace=None, out=None):
+    """y = conv(x, w) + b as the fused implicit-GEMM convolution.
+
+    PRE_REORDER: K3 packs the split weights in tap order (skipped when `packed` =
+    (w_hi, w_lo, w_f32) is given); IN_PACKING: K0 splits the activations once into the
+    NHWC workspace (TMA path only); IN_MICROKERNEL: the persistent tcgen05 kernel (TMA im2col
+    tiles, TMEM accumulation, NCHW epilogue with bias)."""
     ledger = ledger if ledger is not None else PhaseLedger()
     torch = _torch()
     lib = _capi.load()
@@ -406,14 +454,30 @@ def conv_fused(inputs, ledger=None, *, variant: str = DEFAULT_VARIANT, packed=No
     oh, ow = output_shape(d)
     x, host = _dev(inputs.input)
     b = _dev(inputs.bias)[0] if inputs.bias is not None else None
-    y = torch.empty((d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
+    out_host = out is not None and not out.is_cuda
+    y = out if (out is not None and not out_host) else torch.empty(
+        (d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
+    vid = _capi.variant_id(variant)
+    cd = _cd(d)
     if packed is None:
         w, _ = _dev(inputs.weights)
         with _phase(ledger, Phase.PRE_REORDER):
-            packed = _pack_weights(w, d, variant)
+            packed = pack_fused_weights(w, d, variant)
     w_hi, w_lo, w_f32 = packed
+    ws_bytes = fused_layout(d, variant)["workspace_bytes"] if variant in _capi.TC_VARIANTS else 0
+    if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
+    ws_ptr = workspace.data_ptr() if ws_bytes else None
+    st = _stream()
+    if ws_bytes:
+        with _phase(ledger, Phase.IN_PACKING):
+            _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), x.data_ptr(), ws_ptr,
+                                                ws_bytes, st))
     with _phase(ledger, Phase.IN_MICROKERNEL):
-        _capi.check(lib.cb_conv_fused(_capi.variant_id(variant), ctypes.byref(_cd(d)),
-                                      x.data_ptr(), _ptr(w_hi), _ptr(w_lo), _ptr(w_f32), _ptr(b),
-                                      y.data_ptr(), _stream()))
+        _capi.check(lib.cb_conv_fused_packed(vid, ctypes.byref(cd), x.data_ptr(), ws_ptr, ws_bytes,
+                                             _ptr(w_hi), _ptr(w_lo), _ptr(w_f32), _ptr(b),
+                                             y.data_ptr(), st))
+    if out_host:  # D2H into the caller's (pinned) host buffer, stream ordered
+        out.copy_(y, non_blocking=True)
+        return out
     return _host_result(y, host, inputs.input)

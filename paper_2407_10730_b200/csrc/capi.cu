@@ -3,6 +3,7 @@
 // Validation mirrors the reference's data-model checks (ConvDescriptor.__post_init__,
 // descriptor.py:45-59; output_shape, descriptor.py:84-92; ConvInputs shape checks,
 // algos.py:47-59) so that status codes map 1:1 onto the reference exception types.
+#include <atomic>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -18,7 +19,10 @@ int fail(int code, const std::string& msg) {
     g_last_error = msg;
     return code;
 }
+static std::atomic<uint64_t> g_launches{0};
+
 int check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return fail(CB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -99,6 +103,15 @@ int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float
 int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count,
                   const float* acc, const float* bias, float* y, cudaStream_t st);
 int tc_plan_query(const Geom& g, int64_t npix, bool bf16, bool allow_split, cb_tile_plan* out);
+int tma_plan_query(const Geom& g, bool bf16, cb_tile_plan* out);
+FusedLayout fused_layout(const Geom& g, bool bf16);
+int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
+                     cudaStream_t st);
+int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
+                             void* hi, void* lo, cudaStream_t st);
+int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* act_hi,
+                    const void* act_lo, const void* w_hi, const void* w_lo, const float* bias,
+                    float* y, cudaStream_t st);
 int ffma_plan_query(const Geom& g, int64_t npix, bool allow_split, cb_tile_plan* out);
 int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
               const void* w_lo, const float* bias, float* out, int add_mode, int zero_kind,
@@ -169,6 +182,8 @@ extern "C" {
 int cb_version(void) { return CB_ABI_VERSION; }
 
 const char* cb_last_error_string(void) { return cb::g_last_error.c_str(); }
+
+uint64_t cb_launch_count(void) { return cb::g_launches.load(std::memory_order_relaxed); }
 
 int cb_device_sm_count(int* n) {
     if (!n) return fail(CB_ERR_INVALID, "null out pointer");
@@ -358,19 +373,129 @@ int cb_unpack_f32(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t firs
                          (cudaStream_t)stream);
 }
 
-int cb_conv_fused(int variant, const cb_conv_desc* d, const float* x, const void* w_hi,
-                  const void* w_lo, const float* w_f32, const float* bias, float* y,
-                  void* stream) {
-    Geom g;
-    int rc = make_geom(d, &g);
+static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout* L) {
+    int rc = make_geom(d, g);
     if (rc) return rc;
-    if (!x || !y) return fail(CB_ERR_INVALID, "null buffer");
+    if (variant != CB_VARIANT_TC3XTF32 && variant != CB_VARIANT_TC3XBF16 &&
+        variant != CB_VARIANT_FFMA)
+        return fail(CB_ERR_UNSUPPORTED, "unknown variant " + std::to_string(variant));
+    *L = FusedLayout{};
+    if (variant != CB_VARIANT_FFMA) *L = fused_layout(*g, variant == CB_VARIANT_TC3XBF16);
+    return CB_OK;
+}
+
+static void act_halves(const FusedLayout& L, void* ws, void** hi, void** lo) {
+    const size_t half = ((size_t)L.act_elems * L.eb + 255) / 256 * 256;
+    *hi = ws;
+    *lo = static_cast<uint8_t*>(ws) + half;
+}
+
+static int64_t act_ws_bytes(const FusedLayout& L) {
+    if (!L.tma) return 0;
+    return 2 * (((int64_t)L.act_elems * L.eb + 255) / 256 * 256);
+}
+
+int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* out) {
+    Geom g;
+    FusedLayout L;
+    int rc = fused_setup(variant, d, &g, &L);
+    if (rc) return rc;
+    if (!out) return fail(CB_ERR_INVALID, "null out pointer");
+    *out = cb_fused_layout{};
+    out->weight_rows = g.K;
+    if (variant == CB_VARIANT_FFMA) {
+        out->path = 0;
+        out->k_blocks = (g.kdim + 15) / 16;
+        return CB_OK;
+    }
+    out->path = L.tma;
+    out->chunk_channels = L.tma ? L.cb : 0;
+    out->chunk_bytes = L.tma ? L.chunk_bytes : 0;
+    out->k_blocks = L.tma ? L.num_kb : (g.kdim + 128 / L.eb - 1) / (128 / L.eb);
+    out->weight_cols = L.tma ? L.kw_pad : cb_split_kdim(g.kdim);
+    out->workspace_bytes = act_ws_bytes(L);
+    return CB_OK;
+}
+
+int cb_fused_plan_tiles(int variant, const cb_conv_desc* d, cb_tile_plan* plan) {
+    Geom g;
+    FusedLayout L;
+    int rc = fused_setup(variant, d, &g, &L);
+    if (rc) return rc;
+    if (!plan) return fail(CB_ERR_INVALID, "null out pointer");
+    if (variant == CB_VARIANT_FFMA) return ffma_plan_query(g, g.npix, true, plan);
+    if (L.tma) return tma_plan_query(g, variant == CB_VARIANT_TC3XBF16, plan);
+    return tc_plan_query(g, g.npix, variant == CB_VARIANT_TC3XBF16, true, plan);
+}
+
+int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, void* w_hi,
+                          void* w_lo, void* stream) {
+    Geom g;
+    FusedLayout L;
+    int rc = fused_setup(variant, d, &g, &L);
+    if (rc) return rc;
+    if (variant == CB_VARIANT_FFMA)
+        return fail(CB_ERR_INVALID, "the FFMA variant consumes raw OIHW weights");
+    if (!w || !w_hi || !w_lo) return fail(CB_ERR_INVALID, "null buffer");
+    const bool bf16 = variant == CB_VARIANT_TC3XBF16;
+    if (L.tma)
+        return launch_weight_split_taps(bf16, g, L.cb, L.chk, L.kw_pad, w, w_hi, w_lo,
+                                        (cudaStream_t)stream);
+    return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
+                               (cudaStream_t)stream);
+}
+
+int cb_fused_pack_input(int variant, const cb_conv_desc* d, const float* x, void* ws,
+                        size_t ws_bytes, void* stream) {
+    Geom g;
+    FusedLayout L;
+    int rc = fused_setup(variant, d, &g, &L);
+    if (rc) return rc;
+    if (variant == CB_VARIANT_FFMA || !L.tma) return CB_OK;
+    if (!x || !ws) return fail(CB_ERR_INVALID, "null buffer");
+    if ((int64_t)ws_bytes < act_ws_bytes(L))
+        return fail(CB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(act_ws_bytes(L)) +
+                                          " bytes");
+    void *hi, *lo;
+    act_halves(L, ws, &hi, &lo);
+    return launch_act_split(variant == CB_VARIANT_TC3XBF16, g, L.c_alloc, x, hi, lo,
+                            (cudaStream_t)stream);
+}
+
+int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, const void* ws,
+                         size_t ws_bytes, const void* w_hi, const void* w_lo, const float* w_f32,
+                         const float* bias, float* y, void* stream) {
+    Geom g;
+    FusedLayout L;
+    int rc = fused_setup(variant, d, &g, &L);
+    if (rc) return rc;
+    if (!y) return fail(CB_ERR_INVALID, "null output");
     if (d->has_bias && !bias) return fail(CB_ERR_INVALID, "descriptor has bias but bias is null");
+    const float* b = d->has_bias ? bias : nullptr;
+    if (variant != CB_VARIANT_FFMA && L.tma) {
+        if (!ws || (int64_t)ws_bytes < act_ws_bytes(L))
+            return fail(CB_ERR_WORKSPACE, "workspace too small: need " +
+                                              std::to_string(act_ws_bytes(L)) + " bytes");
+        if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need packed weights");
+        void *hi, *lo;
+        act_halves(L, const_cast<void*>(ws), &hi, &lo);
+        return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, g, L, hi, lo, w_hi, w_lo, b, y,
+                               (cudaStream_t)stream);
+    }
+    if (!x) return fail(CB_ERR_INVALID, "null input");
     PixMap pm = full_range(g);
     pm.src_mode = SRC_CONV;
     pm.dst_mode = DST_NCHW;
-    return run_variant(variant, g, pm, x, w_hi, w_lo, w_f32, d->has_bias ? bias : nullptr, y, 0,
+    return run_variant(variant, g, pm, x, w_hi, w_lo, w_f32, b, y, 0,
                        /*zero_kind=NCHW bias fill*/ 1, (cudaStream_t)stream);
+}
+
+int cb_conv_fused(int variant, const cb_conv_desc* d, const float* x, const void* w_hi,
+                  const void* w_lo, const float* w_f32, const float* bias, float* y, void* ws,
+                  size_t ws_bytes, void* stream) {
+    int rc = cb_fused_pack_input(variant, d, x, ws, ws_bytes, stream);
+    if (rc) return rc;
+    return cb_conv_fused_packed(variant, d, x, ws, ws_bytes, w_hi, w_lo, w_f32, bias, y, stream);
 }
 
 }  // extern "C"

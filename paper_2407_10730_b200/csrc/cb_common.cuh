@@ -109,6 +109,26 @@ __device__ __forceinline__ void dst_linear(const Geom& g, const PixMap& pm, int6
     }
 }
 
+// ------------------------------------------------------------------------------------
+// Reduction layout of the TMA-fed fused conv (conv_tma.cu).  The reduction runs over
+// (tap r*S+s, channel chunk cb, channel ci) with CB channels per chunk; one pipeline stage
+// is 128 bytes of reduction per pixel row = cps chunks.  Activations live in an NHWC
+// split workspace with a c_alloc channel pitch (16-byte aligned pixels).
+// ------------------------------------------------------------------------------------
+struct FusedLayout {
+    int tma;           // 1: TMA im2col path usable, 0: use the gather kernel
+    int eb;            // operand bytes: 4 (tf32) / 2 (bf16)
+    int c_alloc;       // NHWC channel pitch (elements)
+    int cb;            // channels per chunk (power of two)
+    int chunk_bytes;   // cb * eb: 16, 32, 64 or 128
+    int chk;           // chunks per tap
+    int cps;           // chunks per stage (128 / chunk_bytes)
+    int total_chunks;  // R * S * chk
+    int num_kb;        // pipeline stages (k blocks) per tile
+    int kw_pad;        // weight row length (elements) = num_kb * 128 / eb
+    int64_t act_elems; // N * H * W * c_alloc (per hi / lo buffer)
+};
+
 // first pixel of slice s (slices of one image are consecutive bands of band_rows rows)
 inline int64_t slice_pixel_begin(const Geom& g, int band_rows, int64_t s) {
     const int64_t per_img = (g.P + band_rows - 1) / band_rows;

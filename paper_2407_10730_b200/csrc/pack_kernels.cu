@@ -203,6 +203,107 @@ int launch_fill_bias(int64_t images, int K, int PQ, const float* bias, float* y,
     return check_launch("fill_bias");
 }
 
+// ---------------------------------------------------------------------------------------
+// K0: activation split + NCHW -> NHWC reorder for the TMA-fed fused conv.
+// Every input element is split exactly once (hi = rn(x), lo = rn(x - hi)) and written
+// channel-innermost with a c_alloc pitch (zero padded), the layout TMA im2col mode walks.
+// 32 x 32 (pixel x channel) smem-transposed tiles: reads coalesced along H*W, writes
+// coalesced along the contiguous (pixel, channel) run of the tile.
+// ---------------------------------------------------------------------------------------
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
+                      void* __restrict__ hi_out, void* __restrict__ lo_out) {
+    __shared__ float tile[32][33];
+    const int p0 = blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    const int64_t n = blockIdx.z;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const float* xn = x + n * (int64_t)C * HW;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = c0 + ty + 8 * i;
+        const int p = p0 + tx;
+        tile[ty + 8 * i][tx] = (c < C && p < HW) ? __ldg(xn + (int64_t)c * HW + p) : 0.f;
+    }
+    __syncthreads();
+    const int cw = min(32, c_alloc - c0);
+    const int pw = min(32, HW - p0);
+    const int64_t obase = (n * HW + p0) * (int64_t)c_alloc + c0;
+    for (int e = threadIdx.x; e < 32 * cw; e += 256) {
+        const int pix = e / cw, ch = e - pix * cw;
+        if (pix >= pw) break;
+        const float v = tile[ch][pix];
+        const int64_t o = obase + (int64_t)pix * c_alloc + ch;
+        if (BF16) {
+            const uint16_t h = bf16_rn_bits(v);
+            static_cast<uint16_t*>(hi_out)[o] = h;
+            static_cast<uint16_t*>(lo_out)[o] = bf16_rn_bits(v - bf16_bits_to_f32(h));
+        } else {
+            const Split2 s = split_tf32(v);
+            static_cast<float*>(hi_out)[o] = s.hi;
+            static_cast<float*>(lo_out)[o] = s.lo;
+        }
+    }
+}
+
+// K3 (fused layout): OIHW -> rows K x kw_pad, k = ((r*S + s)*chk + cb)*CB + ci, zero padded,
+// split into hi / lo.  Matches the (tap, channel-chunk) order the TMA im2col walk feeds.
+template <bool BF16>
+__global__ void weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk,
+                                         int kw_pad, const float* __restrict__ w,
+                                         void* __restrict__ hi_out, void* __restrict__ lo_out) {
+    const int64_t total = (int64_t)K * kw_pad;
+    const int per_tap = chk * CB;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(i / kw_pad);
+        const int k = (int)(i - (int64_t)f * kw_pad);
+        const int tap = k / per_tap;
+        const int c = k - tap * per_tap;
+        float v = 0.f;
+        if (tap < R * S && c < cpg) {
+            const int r = tap / S, s = tap - r * S;
+            v = w[(((int64_t)f * cpg + c) * R + r) * S + s];
+        }
+        if (BF16) {
+            const uint16_t h = bf16_rn_bits(v);
+            static_cast<uint16_t*>(hi_out)[i] = h;
+            static_cast<uint16_t*>(lo_out)[i] = bf16_rn_bits(v - bf16_bits_to_f32(h));
+        } else {
+            const Split2 sp = split_tf32(v);
+            static_cast<float*>(hi_out)[i] = sp.hi;
+            static_cast<float*>(lo_out)[i] = sp.lo;
+        }
+    }
+}
+
+int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
+                     cudaStream_t st) {
+    if (g.N == 0) return CB_OK;
+    dim3 grid((unsigned)((g.HW + 31) / 32), (unsigned)((c_alloc + 31) / 32), (unsigned)g.N);
+    if (grid.z > 65535) return fail(CB_ERR_UNSUPPORTED, "batch too large for act_split grid");
+    if (bf16)
+        act_split_nhwc_kernel<true><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo);
+    else
+        act_split_nhwc_kernel<false><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo);
+    return check_launch("act_split_nhwc");
+}
+
+int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
+                             void* hi, void* lo, cudaStream_t st) {
+    const int64_t total = (int64_t)g.K * kw_pad;
+    if (total == 0) return CB_OK;
+    const int grid = grid_for(total, 256);
+    if (bf16)
+        weight_split_taps_kernel<true><<<grid, 256, 0, st>>>(g.K, g.cpg, g.R, g.S, CB, chk,
+                                                              kw_pad, w, hi, lo);
+    else
+        weight_split_taps_kernel<false><<<grid, 256, 0, st>>>(g.K, g.cpg, g.R, g.S, CB, chk,
+                                                               kw_pad, w, hi, lo);
+    return check_launch("weight_split_taps");
+}
+
 int pre_init_output(const Geom& g, const PixMap& pm, int zero_kind, const float* bias, float* out,
                     cudaStream_t st) {
     if (zero_kind == 1) return launch_fill_bias(g.N, g.K, g.PQ, bias, out, st);

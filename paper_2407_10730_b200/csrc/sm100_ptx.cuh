@@ -60,6 +60,21 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// im2col-mode TMA over an NHWC tensor: loads `pixelsPerColumn` pixels starting at input
+// coordinate (w, h, n) (walking the bounding box with the traversal strides), each
+// `channelsPerPixel` channels from c, shifted by the filter-tap offsets (ow, oh).
+__device__ __forceinline__ void tma_load_im2col_4d(void* dst, const CUtensorMap* map,
+                                                   uint64_t* bar, int32_t c, int32_t w,
+                                                   int32_t h, int32_t n, uint16_t ow,
+                                                   uint16_t oh) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)),
+        "h"(ow), "h"(oh)
+        : "memory");
+}
+
 // ---- tcgen05: TMEM ---------------------------------------------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -142,6 +157,22 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
     d |= (uint64_t)2 << 61;
     return d;
 }
+
+// General K-major descriptor: layout 0 = no swizzle (core matrices of 8 rows x 16 B;
+// lbo = byte distance between the two 16 B K halves, sbo = between 8-row groups),
+// 6 = SWIZZLE_32B, 4 = SWIZZLE_64B, 2 = SWIZZLE_128B (sbo = 8 rows x row pitch).
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t smem_addr, uint32_t layout, uint32_t sbo,
+                                            uint32_t lbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar) { mbar_arrive(bar); }
 
 // Instruction descriptor (kind::tf32 / kind::f16 with fp32 accumulate), K-major A and B.
 //   [4,6) c_format=1 (F32) | [7,10) a_format | [10,13) b_format (TF32=2, BF16=1)

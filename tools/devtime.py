@@ -45,9 +45,12 @@ def main(names):
         inp = algos.ConvInputs(desc=d, input=x, weights=w)
         fl = conv_flops(d)
         for v in ("tc3xtf32", "tc3xbf16", "ffma"):
-            packed = algos._pack_weights(w, d, v)
-            t = timeit(lambda: algos.conv_fused(inp, variant=v, packed=packed))
-            print(f"{name:6s} fused/{v:9s} {t*1e6:9.1f} us  {fl/t/1e12:7.2f} TFLOP/s  plan={algos.plan_tiles(d, v)}")
+            packed = algos.pack_fused_weights(w, d, v)
+            ws = algos.fused_workspace(d, v) if v != "ffma" else None
+            y = torch.empty((d.batch, d.out_channels) + tuple(algos.output_shape(d)), device="cuda")
+            t = timeit(lambda: algos.conv_fused(inp, variant=v, packed=packed, workspace=ws, out=y))
+            print(f"{name:6s} fused/{v:9s} {t*1e6:9.1f} us  {fl/t/1e12:7.2f} TFLOP/s  "
+                  f"layout={algos.fused_layout(d, v) if v != 'ffma' else '-'} plan={algos.fused_plan(d, v)}")
         t = timeit(lambda: algos._im2col_dev(x, d))
         print(f"{name:6s} im2col           {t*1e6:9.1f} us  {pack_bytes(d)/t/1e9:7.1f} GB/s")
         for fn in (algos.conv_baseline_im2col_gemm, algos.conv_main_blocked_direct):
@@ -62,5 +65,27 @@ def main(names):
         sys.stdout.flush()
 
 
+def accuracy_vs_k():
+    """Normalized max error of each variant against float64 as the reduction grows."""
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    for c, r in [(64, 1), (256, 1), (1024, 1), (256, 3), (1024, 3), (4096, 1), (2048, 7)]:
+        d = ConvDescriptor(batch=1, in_channels=c, in_h=14, in_w=14, out_channels=64, k_h=r,
+                           k_w=r, pad_h=r // 2, pad_w=r // 2)
+        rng = np.random.default_rng(1)
+        x = (rng.random((1, c, 14, 14), dtype=np.float32) * 2 - 1)
+        w = (rng.random((64, c, r, r), dtype=np.float32) * 2 - 1)
+        ref = torch.nn.functional.conv2d(torch.from_numpy(x).double(), torch.from_numpy(w).double(),
+                                         padding=r // 2).numpy()
+        inp = algos.ConvInputs(desc=d, input=x, weights=w)
+        errs = {}
+        for v in ("tc3xtf32", "tc3xbf16", "ffma"):
+            y = algos.conv_fused(inp, variant=v)
+            errs[v] = float(np.abs(y.astype(np.float64) - ref).max()) / np.sqrt(c * r * r)
+        print(f"acc K={c*r*r:7d} " + " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:] or list(CONFIGS))
+    if sys.argv[1:2] == ["acc"]:
+        accuracy_vs_k()
+    else:
+        main(sys.argv[1:] or list(CONFIGS))
