@@ -33,7 +33,8 @@ stream before it closes so the host clock measures the kernel.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+import functools
+from dataclasses import dataclass, fields
 
 import numpy as np
 
@@ -48,6 +49,7 @@ from .timing import HOST_PHASES, Phase, PhaseLedger
 DEFAULT_VARIANT = "tc3xtf32"
 FUSED_DEFAULT_VARIANT = "tc3xbf16"
 B200_L2_BYTES = 126 * 1024 * 1024
+_DESC_FIELDS = tuple(f.name for f in fields(ConvDescriptor))
 
 __all__ = [
     "CacheParams", "ConvInputs", "GemmBlocking", "UnsupportedDescriptorError",
@@ -179,6 +181,20 @@ class _phase:
 
 def _cd(desc) -> _capi.CbConvDesc:
     return _capi.cdesc(desc)
+
+
+class _NullLedger:
+    """Records nothing and never synchronises (used when the caller passes no ledger)."""
+    device_timed = True
+
+    def start(self, phase) -> None:
+        pass
+
+    def update(self, phase) -> None:
+        pass
+
+
+_NULL_LEDGER = _NullLedger()
 
 
 # ---------------------------------------------------------------------------------------
@@ -402,12 +418,24 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
 # ---------------------------------------------------------------------------------------
 # Fused implicit-GEMM convolution (K6 / K7)
 # ---------------------------------------------------------------------------------------
-def fused_layout(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
-    """cb_fused_layout_query: path (1 = TMA im2col, 0 = gather), chunking, workspace."""
+def _env_key() -> tuple:
+    import os
+    return tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("CB_TMA_")))
+
+
+@functools.lru_cache(maxsize=1024)
+def _fused_layout_cached(desc, variant: str, env: tuple) -> tuple:
     fl = _capi.CbFusedLayout()
     _capi.check(_capi.load().cb_fused_layout_query(_capi.variant_id(variant),
                                                    ctypes.byref(_cd(desc)), ctypes.byref(fl)))
-    return fl.as_dict()
+    return tuple(fl.as_dict().items())
+
+
+def fused_layout(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
+    """cb_fused_layout_query: path (1 = TMA im2col, 0 = gather), chunking, workspace.
+    Cached per (descriptor, variant): it is pure host arithmetic."""
+    return dict(_fused_layout_cached(ConvDescriptor(**{f: getattr(desc, f) for f in _DESC_FIELDS}),
+                                     variant, _env_key()))
 
 
 def fused_plan(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
@@ -481,3 +509,78 @@ def conv_fused(inputs, ledger=None, *, variant: str = FUSED_DEFAULT_VARIANT, pac
         out.copy_(y, non_blocking=True)
         return out
     return _host_result(y, host, inputs.input)
+
+
+class FusedConv:
+    """Plan-once fused convolution for one descriptor (the cuDNN/cuBLASLt "plan" idiom).
+
+    Layout, packed-weight buffers and the K0 workspace are created once; run() only
+    launches K3 (optional), K0 and K6.  capture() records a whole step into a CUDA graph
+    bound to fixed buffers, so repeated steps cost one graph launch of host time instead of
+    several ctypes calls (the GPU-native replacement for a tracing compiler).  A FusedConv
+    owns one workspace: do not run the same object concurrently on two streams."""
+
+    def __init__(self, desc, variant: str = FUSED_DEFAULT_VARIANT, device="cuda"):
+        torch = _torch()
+        self.desc = desc
+        self.variant = variant
+        self.vid = _capi.variant_id(variant)
+        self._cd = _cd(desc)
+        self._lib = _capi.load()
+        oh, ow = output_shape(desc)
+        self.out_shape = (desc.batch, desc.out_channels, oh, ow)
+        self.device = torch.device(device)
+        self.layout = fused_layout(desc, variant) if variant in _capi.TC_VARIANTS else None
+        self.w_hi = self.w_lo = self.w_f32 = None
+        if self.layout is not None:
+            dt = torch.float32 if variant == "tc3xtf32" else torch.int16
+            shape = (self.layout["weight_rows"], self.layout["weight_cols"])
+            self.w_hi = torch.empty(shape, dtype=dt, device=self.device)
+            self.w_lo = torch.empty(shape, dtype=dt, device=self.device)
+        self.ws_bytes = self.layout["workspace_bytes"] if self.layout else 0
+        self.workspace = (torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+                          if self.ws_bytes else None)
+
+    def pack_weights(self, w_dev) -> None:
+        """K3: OIHW weights -> the packed split halves this plan's kernel reads."""
+        if self.layout is None:
+            self.w_f32 = w_dev.reshape(self.desc.out_channels, -1).contiguous()
+            return
+        _capi.check(self._lib.cb_fused_pack_weights(self.vid, ctypes.byref(self._cd),
+                                                    w_dev.data_ptr(), self.w_hi.data_ptr(),
+                                                    self.w_lo.data_ptr(), _stream()))
+
+    def run(self, x_dev, y_dev, bias_dev=None, ledger=None, weights=None):
+        """One step on device buffers: [K3 if `weights` is given] -> K0 -> K6.  Without a
+        ledger nothing is timed and nothing synchronises (safe under graph capture)."""
+        ledger = ledger if ledger is not None else _NULL_LEDGER
+        st = _stream()
+        if weights is not None:
+            with _phase(ledger, Phase.PRE_REORDER):
+                self.pack_weights(weights)
+        ws = self.workspace.data_ptr() if self.workspace is not None else None
+        if ws is not None:
+            with _phase(ledger, Phase.IN_PACKING):
+                _capi.check(self._lib.cb_fused_pack_input(self.vid, ctypes.byref(self._cd),
+                                                          x_dev.data_ptr(), ws, self.ws_bytes, st))
+        with _phase(ledger, Phase.IN_MICROKERNEL):
+            _capi.check(self._lib.cb_conv_fused_packed(
+                self.vid, ctypes.byref(self._cd), x_dev.data_ptr(), ws, self.ws_bytes,
+                _ptr(self.w_hi), _ptr(self.w_lo), _ptr(self.w_f32), _ptr(bias_dev),
+                y_dev.data_ptr(), st))
+        return y_dev
+
+    def capture(self, x_dev, w_dev, y_dev, bias_dev=None, ledger=None):
+        """CUDA graph of one full step (K3 + K0 + K6) bound to these buffers.  A ledger
+        built with EventLedger(external=True) is captured too: every replay re-records its
+        events, so its snapshot() gives the phase times of the latest replay."""
+        torch = _torch()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside capture (attributes, tensor maps)
+            self.run(x_dev, y_dev, bias_dev, weights=w_dev)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.run(x_dev, y_dev, bias_dev, ledger=ledger, weights=w_dev)
+        return graph

@@ -106,12 +106,15 @@ int tc_plan_query(const Geom& g, int64_t npix, bool bf16, bool allow_split, cb_t
 int tma_plan_query(const Geom& g, bool bf16, cb_tile_plan* out);
 FusedLayout fused_layout(const Geom& g, bool bf16);
 int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
-                     cudaStream_t st);
+                     int* counters, int n_counters, cudaStream_t st);
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
                              void* hi, void* lo, cudaStream_t st);
 int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* act_hi,
                     const void* act_lo, const void* w_hi, const void* w_lo, const float* bias,
-                    float* y, cudaStream_t st);
+                    float* y, void* tail_ws, cudaStream_t st);
+int64_t tma_tail_workspace_bytes(const Geom& g, const FusedLayout& L);
+int debug_trace_copy(unsigned long long* host, int max_ctas, int* slots);
+int tma_tail_counters(const Geom& g, const FusedLayout& L);
 int ffma_plan_query(const Geom& g, int64_t npix, bool allow_split, cb_tile_plan* out);
 int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
               const void* w_lo, const float* bias, float* out, int add_mode, int zero_kind,
@@ -184,6 +187,12 @@ int cb_version(void) { return CB_ABI_VERSION; }
 const char* cb_last_error_string(void) { return cb::g_last_error.c_str(); }
 
 uint64_t cb_launch_count(void) { return cb::g_launches.load(std::memory_order_relaxed); }
+
+// Diagnostics (not in convb200.h): per-CTA globaltimer stamps of the latest fused-conv
+// launch made with CB_TMA_TRACE set.  Returns the CTA count copied.
+int cb_debug_trace(unsigned long long* host, int max_ctas, int* slots) {
+    return cb::debug_trace_copy(host, max_ctas, slots);
+}
 
 int cb_device_sm_count(int* n) {
     if (!n) return fail(CB_ERR_INVALID, "null out pointer");
@@ -384,15 +393,17 @@ static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout*
     return CB_OK;
 }
 
-static void act_halves(const FusedLayout& L, void* ws, void** hi, void** lo) {
+// Fused workspace = [act hi | act lo | tail split-K counters + partials], 256-B aligned parts.
+static void act_halves(const FusedLayout& L, void* ws, void** hi, void** lo, void** tail) {
     const size_t half = ((size_t)L.act_elems * L.eb + 255) / 256 * 256;
     *hi = ws;
     *lo = static_cast<uint8_t*>(ws) + half;
+    *tail = static_cast<uint8_t*>(ws) + 2 * half;
 }
 
-static int64_t act_ws_bytes(const FusedLayout& L) {
+static int64_t act_ws_bytes(const Geom& g, const FusedLayout& L) {
     if (!L.tma) return 0;
-    return 2 * (((int64_t)L.act_elems * L.eb + 255) / 256 * 256);
+    return 2 * (((int64_t)L.act_elems * L.eb + 255) / 256 * 256) + tma_tail_workspace_bytes(g, L);
 }
 
 int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* out) {
@@ -413,7 +424,7 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
     out->chunk_bytes = L.tma ? L.chunk_bytes : 0;
     out->k_blocks = L.tma ? L.num_kb : (g.kdim + 128 / L.eb - 1) / (128 / L.eb);
     out->weight_cols = L.tma ? L.kw_pad : cb_split_kdim(g.kdim);
-    out->workspace_bytes = act_ws_bytes(L);
+    out->workspace_bytes = act_ws_bytes(g, L);
     return CB_OK;
 }
 
@@ -453,13 +464,13 @@ int cb_fused_pack_input(int variant, const cb_conv_desc* d, const float* x, void
     if (rc) return rc;
     if (variant == CB_VARIANT_FFMA || !L.tma) return CB_OK;
     if (!x || !ws) return fail(CB_ERR_INVALID, "null buffer");
-    if ((int64_t)ws_bytes < act_ws_bytes(L))
-        return fail(CB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(act_ws_bytes(L)) +
-                                          " bytes");
-    void *hi, *lo;
-    act_halves(L, ws, &hi, &lo);
+    if ((int64_t)ws_bytes < act_ws_bytes(g, L))
+        return fail(CB_ERR_WORKSPACE, "workspace too small: need " +
+                                          std::to_string(act_ws_bytes(g, L)) + " bytes");
+    void *hi, *lo, *tail;
+    act_halves(L, ws, &hi, &lo, &tail);
     return launch_act_split(variant == CB_VARIANT_TC3XBF16, g, L.c_alloc, x, hi, lo,
-                            (cudaStream_t)stream);
+                            static_cast<int*>(tail), tma_tail_counters(g, L), (cudaStream_t)stream);
 }
 
 int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, const void* ws,
@@ -473,13 +484,13 @@ int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, con
     if (d->has_bias && !bias) return fail(CB_ERR_INVALID, "descriptor has bias but bias is null");
     const float* b = d->has_bias ? bias : nullptr;
     if (variant != CB_VARIANT_FFMA && L.tma) {
-        if (!ws || (int64_t)ws_bytes < act_ws_bytes(L))
+        if (!ws || (int64_t)ws_bytes < act_ws_bytes(g, L))
             return fail(CB_ERR_WORKSPACE, "workspace too small: need " +
-                                              std::to_string(act_ws_bytes(L)) + " bytes");
+                                              std::to_string(act_ws_bytes(g, L)) + " bytes");
         if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need packed weights");
-        void *hi, *lo;
-        act_halves(L, const_cast<void*>(ws), &hi, &lo);
-        return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, g, L, hi, lo, w_hi, w_lo, b, y,
+        void *hi, *lo, *tail;
+        act_halves(L, const_cast<void*>(ws), &hi, &lo, &tail);
+        return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, g, L, hi, lo, w_hi, w_lo, b, y, tail,
                                (cudaStream_t)stream);
     }
     if (!x) return fail(CB_ERR_INVALID, "null input");

@@ -210,97 +210,153 @@ int launch_fill_bias(int64_t images, int K, int PQ, const float* bias, float* y,
 // 32 x 32 (pixel x channel) smem-transposed tiles: reads coalesced along H*W, writes
 // coalesced along the contiguous (pixel, channel) run of the tile.
 // ---------------------------------------------------------------------------------------
+// Splits VEC consecutive values and stores both halves as one 16-byte vector each.
+template <bool BF16, int VEC>
+__device__ __forceinline__ void store_split16(void* hi_out, void* lo_out, int64_t o,
+                                              const float (&v)[VEC]) {
+    if (BF16) {
+        static_assert(!BF16 || VEC == 8, "bf16: 8 values per 16 bytes");
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint16_t h0 = bf16_rn_bits(v[2 * e]), h1 = bf16_rn_bits(v[2 * e + 1]);
+            const uint16_t l0 = bf16_rn_bits(v[2 * e] - bf16_bits_to_f32(h0));
+            const uint16_t l1 = bf16_rn_bits(v[2 * e + 1] - bf16_bits_to_f32(h1));
+            h[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+            l[e] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+        }
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(hi_out) + o) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(lo_out) + o) = make_uint4(l[0], l[1], l[2], l[3]);
+    } else {
+        static_assert(BF16 || VEC == 4, "tf32: 4 values per 16 bytes");
+        float h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const Split2 s = split_tf32(v[e]);
+            h[e] = s.hi;
+            l[e] = s.lo;
+        }
+        *reinterpret_cast<float4*>(static_cast<float*>(hi_out) + o) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(static_cast<float*>(lo_out) + o) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+// 32 pixels x 64 channels per block: coalesced 128-byte reads along H*W into smem, then
+// each thread splits one 16-byte run of channels of one pixel (c_alloc is a multiple of
+// the run length) and writes hi and lo as 16-byte vectors.
 template <bool BF16>
 __global__ void __launch_bounds__(256)
 act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
-                      void* __restrict__ hi_out, void* __restrict__ lo_out) {
-    __shared__ float tile[32][33];
+                      void* __restrict__ hi_out, void* __restrict__ lo_out, int* counters,
+                      int n_counters) {
+    constexpr int VEC = BF16 ? 8 : 4;
+    __shared__ float tile[64][33];
+    // the fused conv's tail split-K counters start every launch at zero
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+        for (int i = threadIdx.x; i < n_counters; i += 256) counters[i] = 0;
     const int p0 = blockIdx.x * 32;
-    const int c0 = blockIdx.y * 32;
+    const int c0 = blockIdx.y * 64;
     const int64_t n = blockIdx.z;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const float* xn = x + n * (int64_t)C * HW;
+    const int p = p0 + tx;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
         const int c = c0 + ty + 8 * i;
-        const int p = p0 + tx;
         tile[ty + 8 * i][tx] = (c < C && p < HW) ? __ldg(xn + (int64_t)c * HW + p) : 0.f;
     }
     __syncthreads();
-    const int cw = min(32, c_alloc - c0);
+    const int cw = min(64, c_alloc - c0);
+    const int nq = cw / VEC;
     const int pw = min(32, HW - p0);
     const int64_t obase = (n * HW + p0) * (int64_t)c_alloc + c0;
-    for (int e = threadIdx.x; e < 32 * cw; e += 256) {
-        const int pix = e / cw, ch = e - pix * cw;
+    for (int e = threadIdx.x; e < 32 * nq; e += 256) {
+        const int pix = e / nq, q = e - pix * nq;
         if (pix >= pw) break;
-        const float v = tile[ch][pix];
-        const int64_t o = obase + (int64_t)pix * c_alloc + ch;
-        if (BF16) {
-            const uint16_t h = bf16_rn_bits(v);
-            static_cast<uint16_t*>(hi_out)[o] = h;
-            static_cast<uint16_t*>(lo_out)[o] = bf16_rn_bits(v - bf16_bits_to_f32(h));
-        } else {
-            const Split2 s = split_tf32(v);
-            static_cast<float*>(hi_out)[o] = s.hi;
-            static_cast<float*>(lo_out)[o] = s.lo;
-        }
+        float v[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] = tile[q * VEC + j][pix];
+        store_split16<BF16, VEC>(hi_out, lo_out, obase + (int64_t)pix * c_alloc + q * VEC, v);
     }
 }
 
 // K3 (fused layout): OIHW -> rows K x kw_pad, k = ((r*S + s)*chk + cb)*CB + ci, zero padded,
 // split into hi / lo.  Matches the (tap, channel-chunk) order the TMA im2col walk feeds.
+// One thread produces one 16-byte run of k (kw_pad is a multiple of 64 elements).
+// Block (channel chunk of WS_CH, out channel f): the chunk's OIHW slice w[f, c0:c0+WS_CH, :, :]
+// is one contiguous run, read coalesced into smem; every tap's WS_CH channels are then
+// contiguous in the output row, written as 16-byte vectors.  Chunk 0 also zeroes the row
+// tail [R*S*per_tap, kw_pad).
+constexpr int WS_CH = 128;
 template <bool BF16>
-__global__ void weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk,
-                                         int kw_pad, const float* __restrict__ w,
-                                         void* __restrict__ hi_out, void* __restrict__ lo_out) {
-    const int64_t total = (int64_t)K * kw_pad;
+__global__ void __launch_bounds__(256)
+weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_pad,
+                         const float* __restrict__ w, void* __restrict__ hi_out,
+                         void* __restrict__ lo_out) {
+    constexpr int VEC = BF16 ? 8 : 4;
+    extern __shared__ float ws_tile[];  // [WS_CH][R*S]
+    const int f = blockIdx.y;
+    const int c0 = blockIdx.x * WS_CH;
+    const int RS = R * S;
     const int per_tap = chk * CB;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int f = (int)(i / kw_pad);
-        const int k = (int)(i - (int64_t)f * kw_pad);
-        const int tap = k / per_tap;
-        const int c = k - tap * per_tap;
-        float v = 0.f;
-        if (tap < R * S && c < cpg) {
-            const int r = tap / S, s = tap - r * S;
-            v = w[(((int64_t)f * cpg + c) * R + r) * S + s];
+    const int nch = min(WS_CH, cpg - c0);  // real channels in this chunk (may be <= 0)
+    const float* src = w + ((int64_t)f * cpg + c0) * RS;
+    for (int i = threadIdx.x; i < max(nch, 0) * RS; i += 256) ws_tile[i] = __ldg(src + i);
+    __syncthreads();
+    const int cw = min(WS_CH, per_tap - c0);  // output channels of this chunk per tap
+    const int nq = cw / VEC;
+    const int64_t row = (int64_t)f * kw_pad;
+    for (int e = threadIdx.x; e < RS * nq; e += 256) {
+        const int tap = e / nq, q = e - tap * nq;
+        float v[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            const int cl = q * VEC + j;
+            v[j] = cl < nch ? ws_tile[cl * RS + tap] : 0.f;
         }
-        if (BF16) {
-            const uint16_t h = bf16_rn_bits(v);
-            static_cast<uint16_t*>(hi_out)[i] = h;
-            static_cast<uint16_t*>(lo_out)[i] = bf16_rn_bits(v - bf16_bits_to_f32(h));
-        } else {
-            const Split2 sp = split_tf32(v);
-            static_cast<float*>(hi_out)[i] = sp.hi;
-            static_cast<float*>(lo_out)[i] = sp.lo;
+        store_split16<BF16, VEC>(hi_out, lo_out, row + (int64_t)tap * per_tap + c0 + q * VEC, v);
+    }
+    if (blockIdx.x == 0) {
+        for (int k = RS * per_tap + threadIdx.x * VEC; k < kw_pad; k += 256 * VEC) {
+            float z[VEC] = {};
+            store_split16<BF16, VEC>(hi_out, lo_out, row + k, z);
         }
     }
 }
 
 int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
-                     cudaStream_t st) {
+                     int* counters, int n_counters, cudaStream_t st) {
     if (g.N == 0) return CB_OK;
-    dim3 grid((unsigned)((g.HW + 31) / 32), (unsigned)((c_alloc + 31) / 32), (unsigned)g.N);
+    dim3 grid((unsigned)((g.HW + 31) / 32), (unsigned)((c_alloc + 63) / 64), (unsigned)g.N);
     if (grid.z > 65535) return fail(CB_ERR_UNSUPPORTED, "batch too large for act_split grid");
+    if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
+        return fail(CB_ERR_MISALIGNED, "activation workspace must be 16-byte aligned");
     if (bf16)
-        act_split_nhwc_kernel<true><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo);
+        act_split_nhwc_kernel<true><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo,
+                                                           counters, n_counters);
     else
-        act_split_nhwc_kernel<false><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo);
+        act_split_nhwc_kernel<false><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo,
+                                                            counters, n_counters);
     return check_launch("act_split_nhwc");
 }
 
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
                              void* hi, void* lo, cudaStream_t st) {
-    const int64_t total = (int64_t)g.K * kw_pad;
-    if (total == 0) return CB_OK;
-    const int grid = grid_for(total, 256);
-    if (bf16)
-        weight_split_taps_kernel<true><<<grid, 256, 0, st>>>(g.K, g.cpg, g.R, g.S, CB, chk,
-                                                              kw_pad, w, hi, lo);
-    else
-        weight_split_taps_kernel<false><<<grid, 256, 0, st>>>(g.K, g.cpg, g.R, g.S, CB, chk,
-                                                               kw_pad, w, hi, lo);
+    if ((int64_t)g.K * kw_pad == 0) return CB_OK;
+    if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
+        return fail(CB_ERR_MISALIGNED, "packed weights must be 16-byte aligned");
+    if (g.K > 65535) return fail(CB_ERR_UNSUPPORTED, "too many output channels for weight pack");
+    const int per_tap = chk * CB;  // multiple of the 16-byte vector (CB >= 16 B / eb)
+    const size_t smem = (size_t)WS_CH * g.RS * sizeof(float);
+    if (smem > 227 * 1024) return fail(CB_ERR_UNSUPPORTED, "kernel too large for weight pack");
+    dim3 grid((unsigned)((per_tap + WS_CH - 1) / WS_CH), (unsigned)g.K);
+    auto kern = bf16 ? weight_split_taps_kernel<true> : weight_split_taps_kernel<false>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
+    }
+    kern<<<grid, 256, smem, st>>>(g.K, g.cpg, g.R, g.S, CB, chk, kw_pad, w, hi, lo);
     return check_launch("weight_split_taps");
 }
 

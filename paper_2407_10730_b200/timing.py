@@ -109,12 +109,15 @@ class EventLedger(PhaseLedger):
     device_timed = True
 
     def __init__(self, stream=None, host_phases: Iterable[Phase] = HOST_PHASES,
-                 clock: Callable[[], int] = time.perf_counter_ns) -> None:
+                 clock: Callable[[], int] = time.perf_counter_ns, external: bool = False) -> None:
         import torch  # plumbing only: events + streams
 
         self._torch = torch
         self._stream = stream
         self._host = frozenset(Phase(p) for p in host_phases)
+        # external events may be recorded inside a CUDA-graph capture: the graph then
+        # re-records them on every replay, so snapshot() reads the latest replay's times
+        self._external = external
         self._pool: list = []
         super().__init__(clock)
 
@@ -130,7 +133,7 @@ class EventLedger(PhaseLedger):
     def _event(self):
         if self._pool:
             return self._pool.pop()
-        return self._torch.cuda.Event(enable_timing=True)
+        return self._torch.cuda.Event(enable_timing=True, external=self._external)
 
     def _cur_stream(self):
         return self._stream if self._stream is not None else self._torch.cuda.current_stream()

@@ -44,6 +44,51 @@ def test_fused_matches_oracle_on_corpus(cuda, variant):
         _check_conv(d, conv_fused(inp, variant=variant), orc.conv_direct_naive(d, x, w, b))
 
 
+@pytest.mark.parametrize("cg,bn", [(1, 64), (1, 128), (1, 256), (2, 128), (2, 256)])
+@pytest.mark.parametrize("variant", ["tc3xtf32", "tc3xbf16"])
+def test_fused_every_tile_config(cuda, variant, cg, bn, monkeypatch):
+    """Force each TMA tile configuration (1-CTA / CTA pair x BN) on ragged shapes:
+    partial pixel tiles, partial channel tiles, batch > 1, stride, padding, groups."""
+    from paper_2407_10730_b200.algos import conv_fused, fused_layout
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    monkeypatch.setenv("CB_TMA_CG", str(cg))
+    monkeypatch.setenv("CB_TMA_BN", str(bn))
+    shapes = SMALL[:10] + [
+        ConvDescriptor(batch=3, in_channels=64, in_h=15, in_w=13, out_channels=200, k_h=3, k_w=3,
+                       pad_h=1, pad_w=1, has_bias=True),
+        ConvDescriptor(batch=2, in_channels=96, in_h=17, in_w=17, out_channels=72, k_h=3, k_w=3,
+                       stride_h=2, stride_w=2, pad_h=1, pad_w=1),
+        ConvDescriptor(batch=5, in_channels=32, in_h=9, in_w=9, out_channels=256, k_h=1, k_w=1),
+        ConvDescriptor(batch=2, in_channels=64, in_h=12, in_w=12, out_channels=64, k_h=3, k_w=3,
+                       pad_h=1, pad_w=1, groups=2),
+    ]
+    n_tma = 0
+    for d in shapes:
+        inp, (x, w, b) = _inputs(d)
+        n_tma += fused_layout(d, variant)["path"]
+        _check_conv(d, conv_fused(inp, variant=variant), orc.conv_direct_naive(d, x, w, b))
+    assert n_tma >= 4
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_fused_tail_split(cuda, cg, monkeypatch):
+    """Grids with more tiles than clusters and a ragged last wave: the tail tiles are
+    split along K and reduced by the last-arriving part (deterministic fixup)."""
+    from paper_2407_10730_b200.algos import conv_fused, fused_plan
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    monkeypatch.setenv("CB_TMA_CG", str(cg))
+    d = ConvDescriptor(batch=80, in_channels=64, in_h=16, in_w=16, out_channels=64, k_h=3,
+                       k_w=3, pad_h=1, pad_w=1, has_bias=True)
+    inp, (x, w, b) = _inputs(d)
+    ref = orc.conv_im2col64(d, x, w, b)
+    y1 = conv_fused(inp)
+    y2 = conv_fused(inp)
+    _check_conv(d, y1, ref)
+    assert np.array_equal(y1, y2), "tail fixup must be deterministic"
+    monkeypatch.setenv("CB_TMA_TAIL", "0")
+    _check_conv(d, conv_fused(inp), ref)
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_im2col_gemm_matches_oracle_on_corpus(cuda, variant):
     from paper_2407_10730_b200.algos import conv_baseline_im2col_gemm

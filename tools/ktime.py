@@ -1,0 +1,84 @@
+"""Kernel-only timing of the fused conv (K6) and its packing kernels, back to back.
+
+    CB_TMA_CG=2 CB_TMA_BN=256 CB_TMA_DEBUG=0 python tools/ktime.py cfg4 [variant]
+Launches are enqueued back to back between two CUDA events, so host overhead is hidden
+whenever a launch takes longer than its host-side call.  Diagnostics only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np
+import torch
+
+from bench import Clocks
+from paper_2407_10730_b200 import _capi, algos
+from paper_2407_10730_b200.configs import CONFIGS, conv_flops
+
+
+def run(name: str, variant: str, reps: int = 20) -> None:
+    d = CONFIGS[name]
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.random((d.batch, d.in_channels, d.in_h, d.in_w), dtype=np.float32) * 2 - 1).cuda()
+    w = torch.from_numpy(rng.random((d.out_channels, d.in_channels, d.k_h, d.k_w), dtype=np.float32) * 2 - 1).cuda()
+    y = torch.empty((d.batch, d.out_channels) + algos.output_shape(d), device="cuda")
+    lib = _capi.load()
+    cd = _capi.cdesc(d)
+    vid = _capi.variant_id(variant)
+    hi, lo, wf = algos.pack_fused_weights(w, d, variant)
+    ws = algos.fused_workspace(d, variant)
+    nbytes = ws.numel() if ws is not None else 0
+    wsp = ws.data_ptr() if ws is not None else None
+    st = torch.cuda.current_stream().cuda_stream
+    ptr = lambda t: None if t is None else t.data_ptr()
+
+    def k0():
+        _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), x.data_ptr(), wsp, nbytes, st))
+
+    def k6():
+        _capi.check(lib.cb_conv_fused_packed(vid, ctypes.byref(cd), x.data_ptr(), wsp, nbytes,
+                                             ptr(hi), ptr(lo), ptr(wf), None, y.data_ptr(), st))
+
+    def k3():
+        _capi.check(lib.cb_fused_pack_weights(vid, ctypes.byref(cd), w.data_ptr(), ptr(hi),
+                                              ptr(lo), st))
+
+    k0()
+    res = {}
+    clk = None
+    for label, fn in (("K3", k3), ("K0", k0), ("K6", k6)):
+        if fn is not k6 and variant == "ffma":
+            continue
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = Clocks(0) if label == "K6" else None
+        if sampler:
+            sampler.__enter__()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__(None, None, None)
+            clk = sampler.summary()
+        res[label] = e0.elapsed_time(e1) / reps * 1e3
+    if clk:
+        print(f"   clocks during K6: {clk}")
+    t6 = res["K6"] * 1e-6
+    env = {k: v for k, v in os.environ.items() if k.startswith("CB_")}
+    print(f"{name} {variant} env={env} plan={algos.fused_plan(d, variant)}")
+    print("   " + " ".join(f"{k}={v:.1f}us" for k, v in res.items()) +
+          f"  K6 {conv_flops(d) / t6 / 1e12:.1f} TFLOP/s", flush=True)
+
+
+if __name__ == "__main__":
+    run(sys.argv[1] if len(sys.argv) > 1 else "cfg4", sys.argv[2] if len(sys.argv) > 2 else "tc3xbf16")
