@@ -221,14 +221,6 @@ def install(ref_harness, main: str = "sconv", variant: str = algos.DEFAULT_VARIA
 def sweep_shard(descs: Sequence[ConvDescriptor], rank: int, world: int,
                 cost: Callable[[ConvDescriptor], float]) -> list[int]:
     """LPT assignment of independent ops to ranks by predicted cost:
-    returns the indices of `descs` that `rank` runs."""
-    import heapq
-    order = sorted(range(len(descs)), key=lambda i: -cost(descs[i]))
-    heap = [(0.0, r) for r in range(world)]
-    mine = []
-    for i in order:
-        load, r = heapq.heappop(heap)
-        if r == rank:
-            mine.append(i)
-        heapq.heappush(heap, (load + cost(descs[i]), r))
-    return sorted(mine)
+    returns the indices of `descs` that `rank` runs (see shard.lpt_assign)."""
+    from .shard import sweep_partition
+    return sweep_partition(descs, world, cost)[rank]

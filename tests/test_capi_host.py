@@ -1,0 +1,145 @@
+"""The C-ABI library on a host without a GPU: it loads, exports exactly the symbols
+include/convb200.h declares, and its host-only entry points (validation, shapes, plans,
+workspace sizing) behave like the reference data model.  No kernel launches here."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2407_10730_b200 import _capi
+from paper_2407_10730_b200.descriptor import ConvDescriptor, InvalidDescriptorError, output_shape
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not _capi.LIB_PATH.exists():
+        from paper_2407_10730_b200.build import build
+        build()
+    return _capi.load()
+
+
+def header_symbols() -> set[str]:
+    text = (ROOT / "include" / "convb200.h").read_text()
+    return set(re.findall(r"^\s*(?:int|int32_t|uint64_t|const char\*)\s+(cb_\w+)\s*\(", text, re.M))
+
+
+def test_exports_match_header(lib):
+    declared = header_symbols()
+    assert declared == set(_capi.EXPORTS), declared ^ set(_capi.EXPORTS)
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(_capi.LIB_PATH)], capture_output=True,
+                        text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (cb_\w+)$", nm, re.M))
+    assert declared <= exported, declared - exported
+    for name in declared:
+        assert hasattr(lib, name)
+
+
+def test_sass_is_sm100a_tcgen05(lib):
+    out = subprocess.run(["cuobjdump", "-sass", str(_capi.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(_capi.LIB_PATH)],
+                                       capture_output=True, text=True).stdout
+    for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM"):
+        assert mnemonic in out, mnemonic
+    assert "UTCHMMA.2CTA" in out and "IM2COL" in out
+
+
+def test_version_and_split_kdim(lib):
+    assert lib.cb_version() == 1
+    assert [_capi.split_kdim(k) for k in (0, 1, 64, 65, 147)] == [0, 64, 64, 128, 192]
+
+
+def _shape(lib, d):
+    oh, ow = ctypes.c_int32(), ctypes.c_int32()
+    _capi.check(lib.cb_output_shape(ctypes.byref(_capi.cdesc(d)), ctypes.byref(oh), ctypes.byref(ow)))
+    return oh.value, ow.value
+
+
+def test_output_shape_matches_descriptor(lib):
+    for kw in (dict(in_h=224, in_w=224, k_h=7, k_w=7, stride_h=2, stride_w=2, pad_h=3, pad_w=3),
+               dict(in_h=9, in_w=8, k_h=3, k_w=3, dil_h=2, dil_w=1, stride_h=2, pad_h=1),
+               dict(in_h=3, in_w=3, k_h=3, k_w=3)):
+        d = ConvDescriptor(batch=1, in_channels=4, out_channels=4, **kw)
+        assert _shape(lib, d) == output_shape(d)
+
+
+def test_invalid_descriptors_raise_reference_types(lib):
+    bad = _capi.CbConvDesc(1, 4, 2, 2, 4, 5, 5, 1, 1, 0, 0, 1, 1, 1, 0)  # kernel does not fit
+    oh, ow = ctypes.c_int32(), ctypes.c_int32()
+    with pytest.raises(InvalidDescriptorError, match="does not fit"):
+        _capi.check(lib.cb_output_shape(ctypes.byref(bad), ctypes.byref(oh), ctypes.byref(ow)))
+    bad = _capi.CbConvDesc(1, 6, 8, 8, 4, 3, 3, 1, 1, 0, 0, 1, 1, 4, 0)  # groups do not divide
+    with pytest.raises(InvalidDescriptorError):
+        _capi.check(lib.cb_output_shape(ctypes.byref(bad), ctypes.byref(oh), ctypes.byref(ow)))
+
+
+def test_sconv_rejects_groups_and_dilation(lib):
+    for kw in (dict(groups=2), dict(dil_h=2, dil_w=2)):
+        d = ConvDescriptor(batch=1, in_channels=4, in_h=9, in_w=9, out_channels=4, k_h=3, k_w=3, **kw)
+        sp = _capi.CbSlicePlan()
+        with pytest.raises(_capi.UnsupportedDescriptorError, match="groups == 1 and dilation == 1"):
+            _capi.check(lib.cb_sconv_plan(ctypes.byref(_capi.cdesc(d)), 64, ctypes.byref(sp)))
+
+
+def test_sconv_plan_and_ranges(lib):
+    d = ConvDescriptor(batch=3, in_channels=8, in_h=10, in_w=10, out_channels=4, k_h=3, k_w=3,
+                       pad_h=1, pad_w=1)
+    cd = _capi.cdesc(d)
+    sp = _capi.CbSlicePlan()
+    _capi.check(lib.cb_sconv_plan(ctypes.byref(cd), 30, ctypes.byref(sp)))
+    assert (sp.band_rows, sp.num_slices) == (3, 3 * 4)  # ceil(10/3) bands per image
+    jb, jc = ctypes.c_int64(), ctypes.c_int64()
+    covered = 0
+    for first in range(sp.num_slices):
+        _capi.check(lib.cb_sconv_range(ctypes.byref(cd), ctypes.byref(sp), first, 1,
+                                       ctypes.byref(jb), ctypes.byref(jc)))
+        assert jb.value == covered  # slices tile the pixel range contiguously
+        covered += jc.value
+    assert covered == 3 * 100
+    with pytest.raises(InvalidDescriptorError):
+        _capi.check(lib.cb_sconv_range(ctypes.byref(cd), ctypes.byref(sp), 11, 2,
+                                       ctypes.byref(jb), ctypes.byref(jc)))
+
+
+def test_workspace_and_layouts(lib):
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.configs import CONFIGS
+    d = CONFIGS["cfg4"]
+    n = ctypes.c_size_t()
+    _capi.check(lib.cb_workspace_bytes(ctypes.byref(_capi.cdesc(d)), 0, None, ctypes.byref(n)))
+    assert n.value == 4 * 2304 * 25088  # the im2col matrix
+    lay = algos.fused_layout(d, "tc3xbf16")
+    assert lay["path"] == 1 and lay["chunk_bytes"] == 128 and lay["weight_cols"] == 2304
+    assert lay["workspace_bytes"] >= 2 * 2 * 128 * 196 * 256  # NHWC hi + lo bf16
+    lay3 = algos.fused_layout(CONFIGS["cfg3"], "tc3xtf32")
+    assert lay3["path"] == 1 and lay3["chunk_bytes"] == 16  # C=3 padded to 4 channels
+    # depthwise with one channel per group cannot use 16-byte chunks: gather path
+    dw = ConvDescriptor(batch=1, in_channels=8, in_h=9, in_w=9, out_channels=8, k_h=3, k_w=3,
+                        groups=8)
+    assert algos.fused_layout(dw, "tc3xbf16")["path"] == 0
+    plan = algos.fused_plan(d, "tc3xbf16")
+    assert plan["block_m"] in (128, 256) and plan["ctas"] <= 148
+    assert algos.plan_tiles(d, "ffma")["block_n"] == 64
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.descriptor import ConvDescriptor as D
+    import numpy as np
+    d = D(batch=1, in_channels=1, in_h=4, in_w=4, out_channels=1, k_h=3, k_w=3)
+    inp = algos.ConvInputs(desc=d, input=np.zeros((1, 1, 4, 4), np.float32),
+                           weights=np.zeros((1, 1, 3, 3), np.float32))
+    with pytest.raises(_capi.ConvB200Error, match="no CPU fallback"):
+        algos.conv_fused(inp)
