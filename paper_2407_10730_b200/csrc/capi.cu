@@ -96,6 +96,8 @@ int make_geom(const cb_conv_desc* d, Geom* g) {
     return CB_OK;
 }
 
+int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
+                       int first_slice, int count, int64_t j_begin, cudaStream_t st);
 int launch_im2col(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
                   int64_t j_begin, int64_t j_count, cudaStream_t st);
 int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float* w, void* hi,
@@ -233,6 +235,9 @@ int cb_im2col_f32(const cb_conv_desc* d, const float* x, float* cols, void* stre
     int rc = make_geom(d, &g);
     if (rc) return rc;
     if (!x || !cols) return fail(CB_ERR_INVALID, "null buffer");
+    // smem-staged band kernel; the per-element kernel covers windows too wide for smem
+    rc = launch_im2col_band(g, x, cols, false, 0, 0, 0, 0, (cudaStream_t)stream);
+    if (rc != CB_ERR_UNSUPPORTED) return rc;
     return launch_im2col(g, x, cols, false, 1, 0, g.npix, (cudaStream_t)stream);
 }
 
@@ -268,6 +273,10 @@ int cb_sconv_pack_f32(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t 
     if (!x || !slices) return fail(CB_ERR_INVALID, "null buffer");
     int64_t jb, jc;
     if ((rc = slice_range(g, plan, first_slice, count, &jb, &jc))) return rc;
+    if (count == 0) return CB_OK;
+    rc = launch_im2col_band(g, x, slices, true, plan->band_rows, first_slice, count, jb,
+                            (cudaStream_t)stream);
+    if (rc != CB_ERR_UNSUPPORTED) return rc;
     return launch_im2col(g, x, slices, true, plan->band_rows, jb, jc, (cudaStream_t)stream);
 }
 

@@ -11,6 +11,8 @@
 // coalesced 16-byte vectors and the loads of a warp walk one input row.  The input is
 // read through L2 once from HBM (every tap re-reads it from L2); the packed matrix is
 // written once: algorithmic bytes = 4 * (N*C*H*W + C*R*S*N*P*Q).
+#include <algorithm>
+
 #include "cb_common.cuh"
 
 namespace cb {
@@ -91,6 +93,213 @@ im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ out, int 
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1/K2 (band kernel): one block = (image n, CC channels, a band of TR output rows).
+// The zero-padded input window of the band -- IR = (TR-1)*sh + (R-1)*dh + 1 rows of
+// W + 2*pw columns per channel -- is staged in smem with coalesced row reads (each input
+// element read from L2 once per block instead of once per tap), then every (c, ky, kx)
+// packed row of the band is written as one contiguous run of TR*Q pixels: one LDS and one
+// coalesced STG per output element.  The kernel is HBM-write bound.
+//   SLICED = false: dst = cols[row][j]               (im2col_transform layout)
+//   SLICED = true : dst = slice buffer of the chunk  (band never crosses a slice)
+// ---------------------------------------------------------------------------------------
+constexpr int BAND_THREADS = 256;
+constexpr int BAND_MAXM = 8;  // pixels per band <= BAND_THREADS * BAND_MAXM
+
+struct BandPlan {
+    int TR;            // output rows per band
+    int CC;            // channels per block
+    int IR, IWp;       // staged window rows / row pitch
+    int bands_per_unit;  // bands per image (K1) or per slice (K2)
+    int PXT;             // pixels of a full band (offset-table size)
+    size_t smem;
+};
+
+template <bool SLICED>
+__global__ void __launch_bounds__(BAND_THREADS)
+im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __restrict__ out,
+                   int band_rows, int first_slice, int64_t j_begin) {
+    extern __shared__ float smem_band[];  // [pixel offset table][CC][IR][IWp]
+    int* off_tab = reinterpret_cast<int*>(smem_band);
+    float* win = smem_band + (bp.PXT + 3) / 4 * 4;
+    // ---- which band ----
+    const int unit = blockIdx.x / bp.bands_per_unit;  // image (K1) or slice index (K2)
+    const int sub = blockIdx.x - unit * bp.bands_per_unit;
+    int n, y_lo, y_hi;  // output rows [y_lo, y_hi) of image n
+    if (!SLICED) {
+        n = unit;
+        y_lo = sub * bp.TR;
+        y_hi = min(g.P, y_lo + bp.TR);
+    } else {
+        const int per_img = (g.P + band_rows - 1) / band_rows;
+        const int s = first_slice + unit;
+        n = s / per_img;
+        const int s0 = (s - n * per_img) * band_rows;
+        const int s1 = min(g.P, s0 + band_rows);
+        y_lo = s0 + sub * bp.TR;
+        y_hi = min(s1, y_lo + bp.TR);
+    }
+    if (y_lo >= y_hi) return;  // block-uniform
+    const int c0 = blockIdx.y * bp.CC;
+    const int cc = min(bp.CC, g.C - c0);
+    const int npx = (y_hi - y_lo) * g.Q;
+    const int iy0 = y_lo * g.sh - g.ph;
+    const int ir = (y_hi - y_lo - 1) * g.sh + (g.R - 1) * g.dh + 1;
+    // ---- stage the zero-padded window [cc][ir][IWp] (this band's own row count, so the
+    //      smem index of element e is e); (c, r, col) advance by counters, no division ----
+    const float* xb = x + ((int64_t)n * g.C + c0) * g.HW;
+    const int tot = cc * ir * bp.IWp;
+    {
+        const int plane = ir * bp.IWp;
+        // BAND_THREADS in the mixed radix (c, r, col) = (., ir, IWp)
+        const int drow = BAND_THREADS / bp.IWp, dcol = BAND_THREADS - drow * bp.IWp;
+        const int dc = drow / ir, dr = drow - dc * ir;
+        int e = threadIdx.x;
+        int c = e / plane;
+        int r = (e - c * plane) / bp.IWp;
+        int col = e - c * plane - r * bp.IWp;
+        while (e < tot) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int iy = iy0 + r, ix = col - g.pw;
+                v[u] = 0.f;
+                if (e + u * BAND_THREADS < tot && (unsigned)iy < (unsigned)g.H &&
+                    (unsigned)ix < (unsigned)g.W)
+                    v[u] = __ldg(xb + (int64_t)c * g.HW + iy * g.W + ix);
+                col += dcol;
+                r += dr;
+                c += dc;
+                if (col >= bp.IWp) { col -= bp.IWp; ++r; }
+                if (r >= ir) { r -= ir; ++c; }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (e + u * BAND_THREADS < tot) win[e + u * BAND_THREADS] = v[u];
+            e += 8 * BAND_THREADS;
+        }
+    }
+    // ---- pixel -> window offset table (the same for every packed row of the band) and
+    //      packed row -> window base table (no integer division in the store loop) ----
+    int* row_tab = off_tab + (bp.PXT + 3) / 4 * 4 + bp.CC * bp.IR * bp.IWp;
+    for (int pix = threadIdx.x; pix < npx; pix += BAND_THREADS) {
+        const int oyl = pix / g.Q;
+        off_tab[pix] = oyl * g.sh * bp.IWp + (pix - oyl * g.Q) * g.sw;
+    }
+    const int nrows = cc * g.RS;
+    for (int r = threadIdx.x; r < nrows; r += BAND_THREADS) {
+        const int c = r / g.RS;
+        const int t = r - c * g.RS;
+        const int ky = t / g.S, kx = t - (t / g.S) * g.S;
+        row_tab[r] = (c * ir + ky * g.dh) * bp.IWp + kx * g.dw;
+    }
+    __syncthreads();
+    // ---- destination of this band's run in every packed row ----
+    const int64_t jband = (int64_t)n * g.PQ + (int64_t)y_lo * g.Q;
+    int64_t row_stride, dst0;
+    if (!SLICED) {
+        row_stride = g.npix;
+        dst0 = jband;
+    } else {
+        const int per_img = (g.P + band_rows - 1) / band_rows;
+        const int s = first_slice + unit;
+        const int s0 = (s - (s / per_img) * per_img) * band_rows;
+        const int np = (min(g.P, s0 + band_rows) - s0) * g.Q;
+        const int64_t j0 = (int64_t)n * g.PQ + (int64_t)s0 * g.Q;
+        row_stride = np;
+        dst0 = (int64_t)g.kdim * (j0 - j_begin) + (jband - j0);
+    }
+    // ---- each warp streams 4 packed rows (c, ky, kx) per pass; one offset-table load
+    //      feeds 4 gathers and 4 coalesced stores ----
+    constexpr int NW = BAND_THREADS / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* const out_b = out + dst0 + (int64_t)c0 * g.RS * row_stride;
+    for (int r0 = warp * 4; r0 < nrows; r0 += 4 * NW) {
+        const int nr = min(4, nrows - r0);  // warp-uniform
+        const float* w0 = win + row_tab[r0];
+        const float* w1 = win + row_tab[min(r0 + 1, nrows - 1)];
+        const float* w2 = win + row_tab[min(r0 + 2, nrows - 1)];
+        const float* w3 = win + row_tab[min(r0 + 3, nrows - 1)];
+        float* d0 = out_b + (int64_t)r0 * row_stride;
+        float* d1 = d0 + row_stride;
+        float* d2 = d1 + row_stride;
+        float* d3 = d2 + row_stride;
+        if (nr == 4) {
+#pragma unroll 2
+            for (int pix = lane; pix < npx; pix += 32) {
+                const int o = off_tab[pix];
+                const float v0 = w0[o], v1 = w1[o], v2 = w2[o], v3 = w3[o];
+                d0[pix] = v0;
+                d1[pix] = v1;
+                d2[pix] = v2;
+                d3[pix] = v3;
+            }
+        } else {
+            for (int pix = lane; pix < npx; pix += 32) {
+                const int o = off_tab[pix];
+                d0[pix] = w0[o];
+                if (nr > 1) d1[pix] = w1[o];
+                if (nr > 2) d2[pix] = w2[o];
+            }
+        }
+    }
+}
+
+// Band geometry: ~1-2K pixels per band (<= BAND_THREADS * BAND_MAXM), window <= 40 KB.
+static bool band_plan(const Geom& g, int max_rows, int64_t units, BandPlan* bp) {
+    const int cap_px = BAND_THREADS * BAND_MAXM;
+    if (g.Q > cap_px) return false;
+    int tr = std::max(1, std::min(max_rows, 1536 / std::max(1, g.Q)));
+    tr = std::min(tr, std::max(1, cap_px / g.Q));
+    auto per_ch_of = [&](int t) {
+        return (size_t)((t - 1) * g.sh + (g.R - 1) * g.dh + 1) * (g.W + 2 * g.pw) * sizeof(float);
+    };
+    // ~16 KB windows keep ~8 blocks (64 warps) resident per SM, so one block's staging
+    // loads overlap the other blocks' streaming stores
+    int cc = (int)std::max<size_t>(1, std::min<size_t>(g.C, (16 * 1024) / per_ch_of(tr)));
+    // at least ~2 waves of blocks: shrink the channel group, then the band (>= 256 px)
+    static const int waves = [] {
+        const char* e = getenv("CB_BAND_WAVES");
+        return e ? atoi(e) : 0;
+    }();
+    const int64_t want = (int64_t)waves * sm_count() * 8;
+    auto blocks = [&](int t, int c) {
+        return units * ((max_rows + t - 1) / t) * ((g.C + c - 1) / c);
+    };
+    while (blocks(tr, cc) < want && cc > 1) cc = (cc + 1) / 2;
+    while (blocks(tr, cc) < want && tr > 1 && (tr / 2) * g.Q >= 256) tr /= 2;
+    bp->TR = tr;
+    bp->IR = (tr - 1) * g.sh + (g.R - 1) * g.dh + 1;
+    bp->IWp = g.W + 2 * g.pw;
+    const size_t per_ch = per_ch_of(tr);
+    if (per_ch > 96 * 1024) return false;
+    bp->CC = cc;
+    bp->PXT = tr * g.Q;  // offset-table entries (pixels of a full band)
+    bp->smem = per_ch * bp->CC + sizeof(int) * ((bp->PXT + 3) / 4 * 4) +
+               sizeof(int) * (size_t)bp->CC * g.RS;
+    return true;
+}
+
+int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
+                       int first_slice, int count, int64_t j_begin, cudaStream_t st) {
+    BandPlan bp{};
+    const int64_t units = sliced ? count : g.N;
+    if (!band_plan(g, sliced ? band_rows : g.P, units, &bp)) return CB_ERR_UNSUPPORTED;
+    bp.bands_per_unit = ((sliced ? band_rows : g.P) + bp.TR - 1) / bp.TR;
+    const int64_t gx = units * bp.bands_per_unit;
+    const int64_t gy = (g.C + bp.CC - 1) / bp.CC;
+    if (gx > 0x7fffffffLL || gy > 65535) return CB_ERR_UNSUPPORTED;
+    auto kern = sliced ? im2col_band_kernel<true> : im2col_band_kernel<false>;
+    if (bp.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)bp.smem);
+        if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
+    }
+    kern<<<dim3((unsigned)gx, (unsigned)gy), BAND_THREADS, bp.smem, st>>>(
+        g, bp, x, out, band_rows, first_slice, j_begin);
+    return check_launch(sliced ? "sconv_pack_band" : "im2col_band");
 }
 
 // K3: rows x kdim (row-major) -> hi/lo rows x kdim_pad, zero padded.

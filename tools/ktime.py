@@ -80,5 +80,64 @@ def run(name: str, variant: str, reps: int = 20) -> None:
           f"  K6 {conv_flops(d) / t6 / 1e12:.1f} TFLOP/s", flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and (len(sys.argv) < 2 or sys.argv[1] not in ("pack", "ceiling")):
     run(sys.argv[1] if len(sys.argv) > 1 else "cfg4", sys.argv[2] if len(sys.argv) > 2 else "tc3xbf16")
+
+
+def pack(name: str, reps: int = 20) -> None:
+    """K1 (im2col) and K2 (slice pack over all slices) back to back, with GB/s of the
+    algorithmic pack bytes."""
+    from paper_2407_10730_b200.configs import pack_bytes
+    d = CONFIGS[name]
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.random((d.batch, d.in_channels, d.in_h, d.in_w), dtype=np.float32)).cuda()
+    lib = _capi.load()
+    cd = _capi.cdesc(d)
+    oh, ow = algos.output_shape(d)
+    kdim = d.in_channels * d.k_h * d.k_w
+    cols = torch.empty(kdim * d.batch * oh * ow, device="cuda")
+    sp = _capi.CbSlicePlan()
+    _capi.check(lib.cb_sconv_plan(ctypes.byref(cd), oh * ow, ctypes.byref(sp)))
+    st = torch.cuda.current_stream().cuda_stream
+    fns = {"K1 im2col": lambda: _capi.check(lib.cb_im2col_f32(ctypes.byref(cd), x.data_ptr(), cols.data_ptr(), st)),
+           "K2 slices": lambda: _capi.check(lib.cb_sconv_pack_f32(ctypes.byref(cd), ctypes.byref(sp), 0, sp.num_slices,
+                                                                  x.data_ptr(), cols.data_ptr(), st))}
+    for label, fn in fns.items():
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps * 1e-3
+        print(f"{name} {label}: {t * 1e6:8.1f} us  {pack_bytes(d) / t / 1e9:7.0f} GB/s", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "pack":
+    for c in sys.argv[2:] or list(CONFIGS):
+        pack(c)
+
+
+def write_ceiling(nbytes: int = 231 << 20, reps: int = 20) -> None:
+    """Plain streaming-write and copy bandwidth on a buffer the size of cfg4's im2col."""
+    a = torch.empty(nbytes // 4, device="cuda")
+    b = torch.empty_like(a)
+    for label, fn, mult in (("fill", lambda: a.fill_(1.0), 1), ("copy", lambda: b.copy_(a), 2)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps * 1e-3
+        print(f"{label} {nbytes >> 20} MB: {t * 1e6:.1f} us  {mult * nbytes / t / 1e9:.0f} GB/s", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ceiling":
+    write_ceiling()
