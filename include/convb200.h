@@ -84,6 +84,15 @@ int         cb_device_sm_count(int* sm_count);
 /* Total kernels this library has launched in the process (for launch accounting). */
 uint64_t    cb_launch_count(void);
 
+/* ---- phase timing (replaces PhaseLedger's host clock, timing.py:28-151) -------------
+ * Timing-enabled CUDA events as opaque handles, recorded on the caller's stream.  The
+ * device-timed ledger brackets each phase with a pair; elapsed_ns waits for `end`.
+ * `external` = 1 records inside a CUDA-graph capture (the graph re-records on replay). */
+int cb_event_create(void** event);
+int cb_event_destroy(void* event);
+int cb_event_record(void* event, void* stream, int external);
+int cb_event_elapsed_ns(void* start, void* end, int64_t* ns);
+
 /* output_shape (descriptor.py:84-92) with the same validation as ConvDescriptor. */
 int cb_output_shape(const cb_conv_desc* d, int32_t* out_h, int32_t* out_w);
 

@@ -24,6 +24,7 @@ TC_VARIANTS = ("tc3xtf32", "tc3xbf16")
 # Every symbol include/convb200.h declares (tests check the .so exports all of them).
 EXPORTS = (
     "cb_version", "cb_last_error_string", "cb_device_sm_count", "cb_launch_count",
+    "cb_event_create", "cb_event_destroy", "cb_event_record", "cb_event_elapsed_ns",
     "cb_output_shape",
     "cb_workspace_bytes", "cb_im2col_f32", "cb_sconv_plan", "cb_sconv_range",
     "cb_sconv_pack_f32", "cb_plan_tiles",
@@ -80,6 +81,11 @@ _SIGNATURES = {
     "cb_last_error_string": ([], ctypes.c_char_p),
     "cb_device_sm_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "cb_launch_count": ([], ctypes.c_uint64),
+    "cb_event_create": ([ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cb_event_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "cb_event_record": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "cb_event_elapsed_ns": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)],
+                            ctypes.c_int),
     "cb_output_shape": ([_DESC, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], ctypes.c_int),
     "cb_workspace_bytes": ([_DESC, ctypes.c_int, _PLAN, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "cb_im2col_f32": ([_DESC, _P, _P, _P], ctypes.c_int),

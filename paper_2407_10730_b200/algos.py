@@ -183,6 +183,37 @@ def _cd(desc) -> _capi.CbConvDesc:
     return _capi.cdesc(desc)
 
 
+def _norm(desc) -> ConvDescriptor:
+    """Hashable copy of any descriptor-like object (the reference's, or ours)."""
+    if type(desc) is ConvDescriptor:
+        return desc
+    return ConvDescriptor(**{f: getattr(desc, f) for f in _DESC_FIELDS})
+
+
+@dataclass(frozen=True)
+class _Prep:
+    """Host-side preparation of one descriptor, computed once: the drop-ins' timed phases
+    then hold nothing but an event record and one C-ABI call."""
+    pcd: object          # ctypes pointer to the cb_conv_desc
+    vid: int
+    oh: int
+    ow: int
+    kdim: int            # (C/g)*R*S
+    kpad: int            # split width of the weight rows (stepwise variants)
+
+
+@functools.lru_cache(maxsize=4096)
+def _prep_cached(desc: ConvDescriptor, variant: str) -> _Prep:
+    oh, ow = output_shape(desc)
+    kdim = (desc.in_channels // desc.groups) * desc.k_h * desc.k_w
+    return _Prep(pcd=ctypes.pointer(_cd(desc)), vid=_capi.variant_id(variant), oh=oh, ow=ow,
+                 kdim=kdim, kpad=_capi.split_kdim(kdim))
+
+
+def _prep(desc, variant: str) -> _Prep:
+    return _prep_cached(_norm(desc), variant)
+
+
 class _NullLedger:
     """Records nothing and never synchronises (used when the caller passes no ledger)."""
     device_timed = True
@@ -224,6 +255,22 @@ def _pack_weights(w_dev, d, variant: str):
         hi, lo = split_weights(w2d, variant)
         return hi, lo, None
     return None, None, w2d.contiguous()
+
+
+def _weight_buffers(w_dev, d, variant: str, pr: _Prep):
+    """Destination buffers of the stepwise weight split (allocated outside the phases)."""
+    if variant not in _capi.TC_VARIANTS:
+        return None, None, w_dev.reshape(d.out_channels, -1)
+    torch = _torch()
+    dt = torch.float32 if variant == "tc3xtf32" else torch.int16
+    hi = torch.empty((d.out_channels, pr.kpad), dtype=dt, device=w_dev.device)
+    return hi, torch.empty_like(hi), None
+
+
+def _split_into(lib, pr: _Prep, d, w_dev, hi, lo, st) -> None:
+    if hi is not None:
+        _capi.check(lib.cb_weight_split(pr.vid, d.out_channels, pr.kdim, w_dev.data_ptr(),
+                                        hi.data_ptr(), lo.data_ptr(), st))
 
 
 def plan_tiles(desc, variant: str = DEFAULT_VARIANT, pixels: int = 0) -> dict:
@@ -272,17 +319,24 @@ def gemm(a, b, c_out, blocking: GemmBlocking, ledger, *, variant: str = DEFAULT_
     c_is_dev = isinstance(c_out, torch.Tensor) and c_out.is_cuda and c_out.dtype == torch.float32 \
         and c_out.is_contiguous()
     c_d = c_out if c_is_dev else _dev(c_out)[0]
+    a_d = a_d.contiguous()
+    vid = _capi.variant_id(variant)
+    if variant in _capi.TC_VARIANTS:
+        dt = torch.float32 if variant == "tc3xtf32" else torch.int16
+        a_hi = torch.empty((m, _capi.split_kdim(k)), dtype=dt, device=a_d.device)
+        a_lo = torch.empty_like(a_hi)
+        a_f32 = None
+    else:
+        a_hi = a_lo = None
+        a_f32 = a_d
     with _phase(ledger, Phase.IN_PACKING):
-        if variant in _capi.TC_VARIANTS:
-            a_hi, a_lo = split_weights(a_d, variant)
-            a_f32 = None
-        else:
-            a_hi = a_lo = None
-            a_f32 = a_d
+        if a_hi is not None:
+            _capi.check(lib.cb_weight_split(vid, m, k, a_d.data_ptr(), a_hi.data_ptr(),
+                                            a_lo.data_ptr(), _stream()))
     with _phase(ledger, Phase.IN_TILING):
         pass  # the GEMM tile plan is computed inside cb_gemm (host side, sub-microsecond)
     with _phase(ledger, Phase.IN_MICROKERNEL):
-        _capi.check(lib.cb_gemm(_capi.variant_id(variant), m, n, k, _ptr(a_hi), _ptr(a_lo),
+        _capi.check(lib.cb_gemm(vid, m, n, k, _ptr(a_hi), _ptr(a_lo),
                                 _ptr(a_f32), b_d.data_ptr(), n, c_d.data_ptr(), n, 1, _stream()))
     with _phase(ledger, Phase.IN_UNPACKING):
         if not c_is_dev:
@@ -300,29 +354,32 @@ def conv_baseline_im2col_gemm(inputs, ledger, blocking: GemmBlocking | None = No
                               variant: str = DEFAULT_VARIANT):
     """Im2col + GEMM (algos.py:185-209): one explicit im2col (PRE_REORDER), weight
     packing (IN_PACKING), tile planning (IN_TILING), then the tensor-core GEMM whose
-    epilogue writes NCHW + bias directly (IN_MICROKERNEL; no post reorder)."""
+    epilogue writes NCHW + bias directly (IN_MICROKERNEL; no post reorder).
+    Buffers are allocated and the host plan prepared before the first phase."""
     _ = blocking if blocking is not None else GemmBlocking()
     torch = _torch()
     lib = _capi.load()
     d = inputs.desc
-    oh, ow = output_shape(d)
+    pr = _prep(d, variant)
     x, host = _dev(inputs.input)
     w, _ = _dev(inputs.weights)
+    w = w.contiguous()
     b = _dev(inputs.bias)[0] if inputs.bias is not None else None
-    y = torch.empty((d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
-    cd = _cd(d)
+    y = torch.empty((d.batch, d.out_channels, pr.oh, pr.ow), dtype=torch.float32, device=x.device)
+    cols = torch.empty((d.in_channels * d.k_h * d.k_w, d.batch * pr.oh * pr.ow),
+                       dtype=torch.float32, device=x.device)
+    w_hi, w_lo, w_f32 = _weight_buffers(w, d, variant, pr)
+    st = _stream()
+    tp = _capi.CbTilePlan()
     with _phase(ledger, Phase.PRE_REORDER):
-        cols = _im2col_dev(x, d)
+        _capi.check(lib.cb_im2col_f32(pr.pcd, x.data_ptr(), cols.data_ptr(), st))
     with _phase(ledger, Phase.IN_PACKING):
-        w_hi, w_lo, w_f32 = _pack_weights(w, d, variant)
+        _split_into(lib, pr, d, w, w_hi, w_lo, st)
     with _phase(ledger, Phase.IN_TILING):
-        tp = _capi.CbTilePlan()
-        _capi.check(lib.cb_plan_tiles(_capi.variant_id(variant), ctypes.byref(cd), 0,
-                                      ctypes.byref(tp)))
+        _capi.check(lib.cb_plan_tiles(pr.vid, pr.pcd, 0, ctypes.byref(tp)))
     with _phase(ledger, Phase.IN_MICROKERNEL):
-        _capi.check(lib.cb_conv_gemm_cols(_capi.variant_id(variant), ctypes.byref(cd),
-                                          cols.data_ptr(), _ptr(w_hi), _ptr(w_lo), _ptr(w_f32),
-                                          _ptr(b), y.data_ptr(), _stream()))
+        _capi.check(lib.cb_conv_gemm_cols(pr.vid, pr.pcd, cols.data_ptr(), _ptr(w_hi), _ptr(w_lo),
+                                          _ptr(w_f32), _ptr(b), y.data_ptr(), st))
     return _host_result(y, host, inputs.input)
 
 
@@ -335,6 +392,11 @@ class SConvPlan:
     num_slices: int
     chunks: tuple[tuple[int, int, int, int], ...]   # (first_slice, count, pix_begin, pix_count)
     max_chunk_pixels: int
+
+
+@functools.lru_cache(maxsize=4096)
+def _plan_sconv_cached(desc: ConvDescriptor, cache: CacheParams) -> SConvPlan:
+    return plan_sconv(desc, cache)
 
 
 def plan_sconv(desc, cache: CacheParams | None = None) -> SConvPlan:
@@ -380,38 +442,39 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
             f"got groups={d.groups}, dilation=({d.dil_h}, {d.dil_w})")
     torch = _torch()
     lib = _capi.load()
-    oh, ow = output_shape(d)
+    pr = _prep(d, variant)
+    cache = cache if cache is not None else CacheParams()
     x, host = _dev(inputs.input)
     w, _ = _dev(inputs.weights)
+    w = w.contiguous()
     b = _dev(inputs.bias)[0] if inputs.bias is not None else None
-    y = torch.empty((d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
-    cd = _cd(d)
-    vid = _capi.variant_id(variant)
-
-    with _phase(ledger, Phase.PRE_ANALYSIS):
-        plan = plan_sconv(d, cache)
-        sp = _capi.CbSlicePlan(plan.band_rows, plan.num_slices)
-    with _phase(ledger, Phase.PRE_REORDER):
-        w_hi, w_lo, w_f32 = _pack_weights(w, d, variant)
-    kdim = d.in_channels * d.k_h * d.k_w
-    slices = torch.empty(kdim * plan.max_chunk_pixels, dtype=torch.float32, device=x.device)
-    acc = torch.empty(d.out_channels * plan.max_chunk_pixels, dtype=torch.float32,
-                      device=x.device)
+    y = torch.empty((d.batch, d.out_channels, pr.oh, pr.ow), dtype=torch.float32, device=x.device)
+    w_hi, w_lo, w_f32 = _weight_buffers(w, d, variant, pr)
     st = _stream()
     tp = _capi.CbTilePlan()
+    with _phase(ledger, Phase.PRE_ANALYSIS):
+        try:
+            plan = _plan_sconv_cached(_norm(d), cache)
+        except TypeError:  # an unhashable caller-side CacheParams
+            plan = plan_sconv(d, cache)
+        sp = _capi.CbSlicePlan(plan.band_rows, plan.num_slices)
+    slices = torch.empty(pr.kdim * plan.max_chunk_pixels, dtype=torch.float32, device=x.device)
+    acc = torch.empty(d.out_channels * plan.max_chunk_pixels, dtype=torch.float32,
+                      device=x.device)
+    psp = ctypes.byref(sp)
+    with _phase(ledger, Phase.PRE_REORDER):
+        _split_into(lib, pr, d, w, w_hi, w_lo, st)
+    xp, sl, ac, yp = x.data_ptr(), slices.data_ptr(), acc.data_ptr(), y.data_ptr()
+    hp, lp, fp, bp = _ptr(w_hi), _ptr(w_lo), _ptr(w_f32), _ptr(b)
     for first, cnt, _jb, jc in plan.chunks:
         with _phase(ledger, Phase.IN_TILING):
-            _capi.check(lib.cb_plan_tiles(vid, ctypes.byref(cd), jc, ctypes.byref(tp)))
+            _capi.check(lib.cb_plan_tiles(pr.vid, pr.pcd, jc, ctypes.byref(tp)))
         with _phase(ledger, Phase.IN_PACKING):
-            _capi.check(lib.cb_sconv_pack_f32(ctypes.byref(cd), ctypes.byref(sp), first, cnt,
-                                              x.data_ptr(), slices.data_ptr(), st))
+            _capi.check(lib.cb_sconv_pack_f32(pr.pcd, psp, first, cnt, xp, sl, st))
         with _phase(ledger, Phase.IN_MICROKERNEL):
-            _capi.check(lib.cb_sconv_gemm(vid, ctypes.byref(cd), ctypes.byref(sp), first, cnt,
-                                          slices.data_ptr(), _ptr(w_hi), _ptr(w_lo), _ptr(w_f32),
-                                          acc.data_ptr(), st))
+            _capi.check(lib.cb_sconv_gemm(pr.vid, pr.pcd, psp, first, cnt, sl, hp, lp, fp, ac, st))
         with _phase(ledger, Phase.IN_UNPACKING):
-            _capi.check(lib.cb_unpack_f32(ctypes.byref(cd), ctypes.byref(sp), first, cnt,
-                                          acc.data_ptr(), _ptr(b), y.data_ptr(), st))
+            _capi.check(lib.cb_unpack_f32(pr.pcd, psp, first, cnt, ac, bp, yp, st))
     return _host_result(y, host, inputs.input)
 
 
@@ -479,32 +542,40 @@ def conv_fused(inputs, ledger=None, *, variant: str = FUSED_DEFAULT_VARIANT, pac
     torch = _torch()
     lib = _capi.load()
     d = inputs.desc
-    oh, ow = output_shape(d)
+    pr = _prep(d, variant)
     x, host = _dev(inputs.input)
     b = _dev(inputs.bias)[0] if inputs.bias is not None else None
     out_host = out is not None and not out.is_cuda
     y = out if (out is not None and not out_host) else torch.empty(
-        (d.batch, d.out_channels, oh, ow), dtype=torch.float32, device=x.device)
-    vid = _capi.variant_id(variant)
-    cd = _cd(d)
-    if packed is None:
-        w, _ = _dev(inputs.weights)
-        with _phase(ledger, Phase.PRE_REORDER):
-            packed = pack_fused_weights(w, d, variant)
-    w_hi, w_lo, w_f32 = packed
-    ws_bytes = fused_layout(d, variant)["workspace_bytes"] if variant in _capi.TC_VARIANTS else 0
+        (d.batch, d.out_channels, pr.oh, pr.ow), dtype=torch.float32, device=x.device)
+    tc = variant in _capi.TC_VARIANTS
+    lay = fused_layout(d, variant) if tc else None
+    ws_bytes = lay["workspace_bytes"] if tc else 0
     if ws_bytes and (workspace is None or workspace.numel() < ws_bytes):
         workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
     ws_ptr = workspace.data_ptr() if ws_bytes else None
     st = _stream()
+    if packed is None:
+        w, _ = _dev(inputs.weights)
+        w = w.contiguous()
+        if tc:
+            dt = torch.float32 if variant == "tc3xtf32" else torch.int16
+            w_hi = torch.empty((lay["weight_rows"], lay["weight_cols"]), dtype=dt, device=x.device)
+            w_lo = torch.empty_like(w_hi)
+            with _phase(ledger, Phase.PRE_REORDER):
+                _capi.check(lib.cb_fused_pack_weights(pr.vid, pr.pcd, w.data_ptr(), w_hi.data_ptr(),
+                                                      w_lo.data_ptr(), st))
+            packed = (w_hi, w_lo, None)
+        else:
+            packed = (None, None, w.reshape(d.out_channels, -1))
+    w_hi, w_lo, w_f32 = packed
+    xp = x.data_ptr()
     if ws_bytes:
         with _phase(ledger, Phase.IN_PACKING):
-            _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), x.data_ptr(), ws_ptr,
-                                                ws_bytes, st))
+            _capi.check(lib.cb_fused_pack_input(pr.vid, pr.pcd, xp, ws_ptr, ws_bytes, st))
     with _phase(ledger, Phase.IN_MICROKERNEL):
-        _capi.check(lib.cb_conv_fused_packed(vid, ctypes.byref(cd), x.data_ptr(), ws_ptr, ws_bytes,
-                                             _ptr(w_hi), _ptr(w_lo), _ptr(w_f32), _ptr(b),
-                                             y.data_ptr(), st))
+        _capi.check(lib.cb_conv_fused_packed(pr.vid, pr.pcd, xp, ws_ptr, ws_bytes, _ptr(w_hi),
+                                             _ptr(w_lo), _ptr(w_f32), _ptr(b), y.data_ptr(), st))
     if out_host:  # D2H into the caller's (pinned) host buffer, stream ordered
         out.copy_(y, non_blocking=True)
         return out

@@ -4,6 +4,7 @@
 // descriptor.py:45-59; output_shape, descriptor.py:84-92; ConvInputs shape checks,
 // algos.py:47-59) so that status codes map 1:1 onto the reference exception types.
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -108,9 +109,9 @@ int tc_plan_query(const Geom& g, int64_t npix, bool bf16, bool allow_split, cb_t
 int tma_plan_query(const Geom& g, bool bf16, cb_tile_plan* out);
 FusedLayout fused_layout(const Geom& g, bool bf16);
 int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
-                     int* counters, int n_counters, cudaStream_t st);
+                     int* counters, int n_counters, cudaStream_t st, int fold);
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
-                             void* hi, void* lo, cudaStream_t st);
+                             void* hi, void* lo, cudaStream_t st, int fold);
 int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* act_hi,
                     const void* act_lo, const void* w_hi, const void* w_lo, const float* bias,
                     float* y, void* tail_ws, cudaStream_t st);
@@ -194,6 +195,40 @@ uint64_t cb_launch_count(void) { return cb::g_launches.load(std::memory_order_re
 // launch made with CB_TMA_TRACE set.  Returns the CTA count copied.
 int cb_debug_trace(unsigned long long* host, int max_ctas, int* slots) {
     return cb::debug_trace_copy(host, max_ctas, slots);
+}
+
+int cb_event_create(void** ev) {
+    if (!ev) return fail(CB_ERR_INVALID, "null out pointer");
+    cudaEvent_t e = nullptr;
+    cudaError_t rc = cudaEventCreateWithFlags(&e, cudaEventDefault);
+    if (rc != cudaSuccess) return fail(CB_ERR_CUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(rc));
+    *ev = e;
+    return CB_OK;
+}
+
+int cb_event_destroy(void* ev) {
+    if (ev) cudaEventDestroy(static_cast<cudaEvent_t>(ev));
+    return CB_OK;
+}
+
+int cb_event_record(void* ev, void* stream, int external) {
+    if (!ev) return fail(CB_ERR_INVALID, "null event");
+    cudaError_t rc = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev),
+                                              static_cast<cudaStream_t>(stream),
+                                              external ? cudaEventRecordExternal : cudaEventRecordDefault);
+    if (rc != cudaSuccess) return fail(CB_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(rc));
+    return CB_OK;
+}
+
+int cb_event_elapsed_ns(void* e0, void* e1, int64_t* ns) {
+    if (!e0 || !e1 || !ns) return fail(CB_ERR_INVALID, "null argument");
+    cudaError_t rc = cudaEventSynchronize(static_cast<cudaEvent_t>(e1));
+    float ms = 0.f;
+    if (rc == cudaSuccess)
+        rc = cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(e0), static_cast<cudaEvent_t>(e1));
+    if (rc != cudaSuccess) return fail(CB_ERR_CUDA, std::string("cudaEventElapsedTime: ") + cudaGetErrorString(rc));
+    *ns = (int64_t)llround((double)ms * 1e6);
+    return CB_OK;
 }
 
 int cb_device_sm_count(int* n) {
@@ -391,7 +426,10 @@ int cb_unpack_f32(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t firs
                          (cudaStream_t)stream);
 }
 
-static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout* L) {
+// g: the descriptor's geometry (K0 reads x with it); gk: the geometry the TMA kernel, its
+// plan and the weight pack run on -- fold_geom(g) when the layout folds, else g.
+static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout* L,
+                       Geom* gk = nullptr) {
     int rc = make_geom(d, g);
     if (rc) return rc;
     if (variant != CB_VARIANT_TC3XTF32 && variant != CB_VARIANT_TC3XBF16 &&
@@ -399,6 +437,7 @@ static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout*
         return fail(CB_ERR_UNSUPPORTED, "unknown variant " + std::to_string(variant));
     *L = FusedLayout{};
     if (variant != CB_VARIANT_FFMA) *L = fused_layout(*g, variant == CB_VARIANT_TC3XBF16);
+    if (gk) *gk = L->fold ? fold_geom(*g) : *g;
     return CB_OK;
 }
 
@@ -416,9 +455,9 @@ static int64_t act_ws_bytes(const Geom& g, const FusedLayout& L) {
 }
 
 int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* out) {
-    Geom g;
+    Geom g, gk;
     FusedLayout L;
-    int rc = fused_setup(variant, d, &g, &L);
+    int rc = fused_setup(variant, d, &g, &L, &gk);
     if (rc) return rc;
     if (!out) return fail(CB_ERR_INVALID, "null out pointer");
     *out = cb_fused_layout{};
@@ -433,73 +472,74 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
     out->chunk_bytes = L.tma ? L.chunk_bytes : 0;
     out->k_blocks = L.tma ? L.num_kb : (g.kdim + 128 / L.eb - 1) / (128 / L.eb);
     out->weight_cols = L.tma ? L.kw_pad : cb_split_kdim(g.kdim);
-    out->workspace_bytes = act_ws_bytes(g, L);
+    out->workspace_bytes = act_ws_bytes(gk, L);
     return CB_OK;
 }
 
 int cb_fused_plan_tiles(int variant, const cb_conv_desc* d, cb_tile_plan* plan) {
-    Geom g;
+    Geom g, gk;
     FusedLayout L;
-    int rc = fused_setup(variant, d, &g, &L);
+    int rc = fused_setup(variant, d, &g, &L, &gk);
     if (rc) return rc;
     if (!plan) return fail(CB_ERR_INVALID, "null out pointer");
     if (variant == CB_VARIANT_FFMA) return ffma_plan_query(g, g.npix, true, plan);
-    if (L.tma) return tma_plan_query(g, variant == CB_VARIANT_TC3XBF16, plan);
+    if (L.tma) return tma_plan_query(gk, variant == CB_VARIANT_TC3XBF16, plan);
     return tc_plan_query(g, g.npix, variant == CB_VARIANT_TC3XBF16, true, plan);
 }
 
 int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, void* w_hi,
                           void* w_lo, void* stream) {
-    Geom g;
+    Geom g, gk;
     FusedLayout L;
-    int rc = fused_setup(variant, d, &g, &L);
+    int rc = fused_setup(variant, d, &g, &L, &gk);
     if (rc) return rc;
     if (variant == CB_VARIANT_FFMA)
         return fail(CB_ERR_INVALID, "the FFMA variant consumes raw OIHW weights");
     if (!w || !w_hi || !w_lo) return fail(CB_ERR_INVALID, "null buffer");
     const bool bf16 = variant == CB_VARIANT_TC3XBF16;
     if (L.tma)
-        return launch_weight_split_taps(bf16, g, L.cb, L.chk, L.kw_pad, w, w_hi, w_lo,
-                                        (cudaStream_t)stream);
+        return launch_weight_split_taps(bf16, gk, L.cb, L.chk, L.kw_pad, w, w_hi, w_lo,
+                                        (cudaStream_t)stream, L.fold);
     return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
                                (cudaStream_t)stream);
 }
 
 int cb_fused_pack_input(int variant, const cb_conv_desc* d, const float* x, void* ws,
                         size_t ws_bytes, void* stream) {
-    Geom g;
+    Geom g, gk;
     FusedLayout L;
-    int rc = fused_setup(variant, d, &g, &L);
+    int rc = fused_setup(variant, d, &g, &L, &gk);
     if (rc) return rc;
     if (variant == CB_VARIANT_FFMA || !L.tma) return CB_OK;
     if (!x || !ws) return fail(CB_ERR_INVALID, "null buffer");
-    if ((int64_t)ws_bytes < act_ws_bytes(g, L))
+    if ((int64_t)ws_bytes < act_ws_bytes(gk, L))
         return fail(CB_ERR_WORKSPACE, "workspace too small: need " +
-                                          std::to_string(act_ws_bytes(g, L)) + " bytes");
+                                          std::to_string(act_ws_bytes(gk, L)) + " bytes");
     void *hi, *lo, *tail;
     act_halves(L, ws, &hi, &lo, &tail);
     return launch_act_split(variant == CB_VARIANT_TC3XBF16, g, L.c_alloc, x, hi, lo,
-                            static_cast<int*>(tail), tma_tail_counters(g, L), (cudaStream_t)stream);
+                            static_cast<int*>(tail), tma_tail_counters(gk, L), (cudaStream_t)stream,
+                            L.fold);
 }
 
 int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, const void* ws,
                          size_t ws_bytes, const void* w_hi, const void* w_lo, const float* w_f32,
                          const float* bias, float* y, void* stream) {
-    Geom g;
+    Geom g, gk;
     FusedLayout L;
-    int rc = fused_setup(variant, d, &g, &L);
+    int rc = fused_setup(variant, d, &g, &L, &gk);
     if (rc) return rc;
     if (!y) return fail(CB_ERR_INVALID, "null output");
     if (d->has_bias && !bias) return fail(CB_ERR_INVALID, "descriptor has bias but bias is null");
     const float* b = d->has_bias ? bias : nullptr;
     if (variant != CB_VARIANT_FFMA && L.tma) {
-        if (!ws || (int64_t)ws_bytes < act_ws_bytes(g, L))
+        if (!ws || (int64_t)ws_bytes < act_ws_bytes(gk, L))
             return fail(CB_ERR_WORKSPACE, "workspace too small: need " +
-                                              std::to_string(act_ws_bytes(g, L)) + " bytes");
+                                              std::to_string(act_ws_bytes(gk, L)) + " bytes");
         if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need packed weights");
         void *hi, *lo, *tail;
         act_halves(L, const_cast<void*>(ws), &hi, &lo, &tail);
-        return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, g, L, hi, lo, w_hi, w_lo, b, y, tail,
+        return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, gk, L, hi, lo, w_hi, w_lo, b, y, tail,
                                (cudaStream_t)stream);
     }
     if (!x) return fail(CB_ERR_INVALID, "null input");

@@ -127,7 +127,28 @@ struct FusedLayout {
     int num_kb;        // pipeline stages (k blocks) per tile
     int kw_pad;        // weight row length (elements) = num_kb * 128 / eb
     int64_t act_elems; // N * H * W * c_alloc (per hi / lo buffer)
+    int fold;          // 0, or the kernel width S when the horizontal taps are folded into
+                       // the channels (small C): the kernel then runs fold_geom(g)
 };
+
+// The same convolution with its S horizontal taps folded into the channel axis: the input
+// becomes [N][H][Q][S*C] (x at column ox*sw + s*dw - pw for channel s*C + c, zero outside)
+// and the kernel an R x 1 conv with unit horizontal stride and no horizontal padding.  Only
+// for groups == 1.  P, Q, K, the reduction length and the output are unchanged.
+inline Geom fold_geom(const Geom& g) {
+    Geom f = g;
+    f.C = g.C * g.S;
+    f.cpg = f.C;
+    f.W = g.Q;
+    f.S = 1;
+    f.sw = 1;
+    f.pw = 0;
+    f.dw = 1;
+    f.HW = f.H * f.W;
+    f.RS = f.R;
+    f.kdim = f.cpg * f.R;
+    return f;
+}
 
 // first pixel of slice s (slices of one image are consecutive bands of band_rows rows)
 inline int64_t slice_pixel_begin(const Geom& g, int band_rows, int64_t s) {

@@ -516,7 +516,7 @@ static int next_pow2(int v) {
     return p;
 }
 
-FusedLayout fused_layout(const Geom& g, bool bf16) {
+static FusedLayout base_layout(const Geom& g, bool bf16) {
     FusedLayout L{};
     L.eb = bf16 ? 2 : 4;
     const int align = 16 / L.eb;      // channels per 16 bytes
@@ -546,6 +546,22 @@ FusedLayout fused_layout(const Geom& g, bool bf16) {
     ok = ok && (g.G == 1 || g.cpg % L.cb == 0);
     ok = ok && (int64_t)g.N * g.HW * L.c_alloc * L.eb < (1LL << 40);
     L.tma = ok ? 1 : 0;
+    return L;
+}
+
+// Fold the horizontal taps into the channels when that shortens the padded reduction
+// (few channels: C=3 pads each tap to a 16-byte chunk, 147 -> 392 for a 7x7 stem; folded
+// it is 7 taps of 21 -> 24 channels, 147 -> 256) -- fewer MMAs and fewer, larger TMA boxes.
+// Weights are repacked to match (weight_split_taps, fold) and K0 writes the folded rows.
+FusedLayout fused_layout(const Geom& g, bool bf16) {
+    FusedLayout L = base_layout(g, bf16);
+    if (g.G == 1 && g.S > 1 && g.C * g.S <= 128 && !std::getenv("CB_NO_FOLD")) {
+        FusedLayout F = base_layout(fold_geom(g), bf16);
+        if (F.tma && (!L.tma || F.num_kb < L.num_kb)) {
+            F.fold = g.S;
+            return F;
+        }
+    }
     return L;
 }
 
@@ -598,8 +614,11 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     TmaPlan& pl = best;
     const int units = sms / pl.cg;
     const int64_t tiles = pl.m_tiles * pl.n_tiles * g.G;
+    // Atomic split-K (bias pre-fill launch + add epilogue) only on request: by default a
+    // short grid is filled by the deterministic tail split below (one launch, no atomics).
     pl.splits = 1;
-    if (tiles < units && L.num_kb >= 4) {
+    const char* splitk = std::getenv("CB_TMA_SPLITK");
+    if (splitk && std::atoi(splitk) == 1 && tiles < units && L.num_kb >= 4) {
         int want = (int)((units + tiles - 1) / tiles);
         pl.splits = std::max(1, std::min(want, L.num_kb / 2));
     }
@@ -608,11 +627,11 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     pl.total_tiles = tiles * pl.splits;
     const int stage_bytes = 2 * TMA_BM * 128 + 2 * (pl.bn / pl.cg) * 128;
     pl.stages = std::min(6, (232448 - 1280) / stage_bytes);
-    pl.grid = (int)std::min<int64_t>(pl.total_tiles, units) * pl.cg;
-    if (const char* gcap = std::getenv("CB_TMA_GRID"))  // diagnostics: cap the persistent grid
-        pl.grid = std::max(pl.cg, std::min(pl.grid, std::atoi(gcap) / pl.cg * pl.cg));
-    // Tail split-K: when whole tiles leave the last wave partly idle, cut each tail tile
-    // into S K-parts (>= 4 stages each) so the last wave fills every cluster.
+    // Tail split-K: when whole tiles leave the last wave partly idle -- or a single short
+    // wave leaves clusters idle -- cut each tail tile into S K-parts so the last wave fills
+    // more clusters.  Parts keep >= 4 K-blocks when the grid is over-full (the fixup must
+    // pay off) and >= 2 on a short grid.  Every item then runs on its own CTA (parts <=
+    // units / tail), so an owner never waits on a part queued behind it.
     pl.full_items = pl.total_tiles;
     pl.total_items = pl.total_tiles;
     pl.tail_tiles = 0;
@@ -620,8 +639,9 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     pl.tail_kbp = L.num_kb;
     const char* no_tail = std::getenv("CB_TMA_TAIL");
     const int64_t tail = tiles % units;
-    if (pl.splits == 1 && tiles > units && tail > 0 && !(no_tail && std::atoi(no_tail) == 0)) {
-        int parts = (int)std::min<int64_t>(std::min<int64_t>(units / tail, L.num_kb / 4),
+    if (pl.splits == 1 && tail > 0 && !(no_tail && std::atoi(no_tail) == 0)) {
+        const int min_kbp = tiles > units ? 4 : 2;
+        int parts = (int)std::min<int64_t>(std::min<int64_t>(units / tail, L.num_kb / min_kbp),
                                            MAX_TAIL_OTHERS + 1);
         if (parts >= 2) {
             pl.tail_kbp = (L.num_kb + parts - 1) / parts;
@@ -632,6 +652,11 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
             pl.total_items = pl.full_items + tail * parts;
         }
     }
+    // One item per cluster at a time: tail parts then all run concurrently (required, an
+    // owner spins on its parts).  The grid cap is a diagnostic for untailed plans only.
+    pl.grid = (int)std::min<int64_t>(pl.total_items, units) * pl.cg;
+    if (const char* gcap = std::getenv("CB_TMA_GRID"); gcap && pl.tail_tiles == 0)
+        pl.grid = std::max(pl.cg, std::min(pl.grid, std::atoi(gcap) / pl.cg * pl.cg));
     return pl;
 }
 

@@ -489,6 +489,39 @@ act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
     }
 }
 
+// K0 for a folded layout (FusedLayout::fold): [N][H][Q][c_alloc] rows whose channel
+// s*C + c holds x[n, c, ih, ox*sw + s*dw - pw] (zero outside the image and past S*C), split
+// into hi / lo.  One thread per 16-byte run; the strided re-reads of x hit L1/L2.
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+act_fold_split_kernel(Geom g, int c_alloc, const float* __restrict__ x, void* __restrict__ hi_out,
+                      void* __restrict__ lo_out, int* counters, int n_counters) {
+    constexpr int VEC = BF16 ? 8 : 4;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < n_counters; i += 256) counters[i] = 0;
+    const int nq = c_alloc / VEC;
+    const int CS = g.C * g.S;
+    const int64_t total = (int64_t)g.N * g.H * g.Q * nq;
+    for (int64_t e = blockIdx.x * 256LL + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+        const int64_t pix = e / nq;  // (n*H + ih)*Q + ox
+        const int q = (int)(e - pix * nq);
+        const int64_t nh = pix / g.Q;
+        const int ox = (int)(pix - nh * g.Q);
+        const int64_t n = nh / g.H;
+        const int ih = (int)(nh - n * g.H);
+        const float* xr = x + (n * g.C * g.H + ih) * (int64_t)g.W;
+        float v[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            const int cp = q * VEC + j;
+            const int s = cp / g.C, c = cp - s * g.C;
+            const int ix = ox * g.sw + s * g.dw - g.pw;
+            v[j] = (cp < CS && (unsigned)ix < (unsigned)g.W) ? __ldg(xr + (int64_t)c * g.HW + ix) : 0.f;
+        }
+        store_split16<BF16, VEC>(hi_out, lo_out, pix * c_alloc + q * VEC, v);
+    }
+}
+
 // K3 (fused layout): OIHW -> rows K x kw_pad, k = ((r*S + s)*chk + cb)*CB + ci, zero padded,
 // split into hi / lo.  Matches the (tap, channel-chunk) order the TMA im2col walk feeds.
 // One thread produces one 16-byte run of k (kw_pad is a multiple of 64 elements).
@@ -501,7 +534,7 @@ template <bool BF16>
 __global__ void __launch_bounds__(256)
 weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_pad,
                          const float* __restrict__ w, void* __restrict__ hi_out,
-                         void* __restrict__ lo_out) {
+                         void* __restrict__ lo_out, int fold) {
     constexpr int VEC = BF16 ? 8 : 4;
     extern __shared__ float ws_tile[];  // [WS_CH][R*S]
     const int f = blockIdx.y;
@@ -509,9 +542,12 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
     const int RS = R * S;
     const int per_tap = chk * CB;
     const int nch = min(WS_CH, cpg - c0);  // real channels in this chunk (may be <= 0)
+    // folded (fold = original S, S == 1 here, one chunk): stage all of w[f] in OIHW order
+    // and read channel c' = s*C + c of tap r from w[f, c, r, s]
     const float* src = w + ((int64_t)f * cpg + c0) * RS;
     for (int i = threadIdx.x; i < max(nch, 0) * RS; i += 256) ws_tile[i] = __ldg(src + i);
     __syncthreads();
+    const int c_orig = fold ? cpg / fold : 0;
     const int cw = min(WS_CH, per_tap - c0);  // output channels of this chunk per tap
     const int nq = cw / VEC;
     const int64_t row = (int64_t)f * kw_pad;
@@ -521,7 +557,12 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
             const int cl = q * VEC + j;
-            v[j] = cl < nch ? ws_tile[cl * RS + tap] : 0.f;
+            if (cl >= nch)
+                v[j] = 0.f;
+            else if (fold)
+                v[j] = ws_tile[(((c0 + cl) % c_orig) * R + tap) * fold + (c0 + cl) / c_orig];
+            else
+                v[j] = ws_tile[cl * RS + tap];
         }
         store_split16<BF16, VEC>(hi_out, lo_out, row + (int64_t)tap * per_tap + c0 + q * VEC, v);
     }
@@ -534,8 +575,22 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
 }
 
 int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
-                     int* counters, int n_counters, cudaStream_t st) {
+                     int* counters, int n_counters, cudaStream_t st, int fold) {
     if (g.N == 0) return CB_OK;
+    if (fold) {
+        if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
+            return fail(CB_ERR_MISALIGNED, "activation workspace must be 16-byte aligned");
+        const int64_t runs = (int64_t)g.N * g.H * g.Q * (c_alloc / (bf16 ? 8 : 4));
+        const int blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (runs + 255) / 256),
+                                                  (int64_t)sm_count() * 16);
+        if (bf16)
+            act_fold_split_kernel<true><<<blocks, 256, 0, st>>>(g, c_alloc, x, hi, lo, counters,
+                                                                 n_counters);
+        else
+            act_fold_split_kernel<false><<<blocks, 256, 0, st>>>(g, c_alloc, x, hi, lo, counters,
+                                                                  n_counters);
+        return check_launch("act_fold_split");
+    }
     dim3 grid((unsigned)((g.HW + 31) / 32), (unsigned)((c_alloc + 63) / 64), (unsigned)g.N);
     if (grid.z > 65535) return fail(CB_ERR_UNSUPPORTED, "batch too large for act_split grid");
     if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
@@ -550,7 +605,9 @@ int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void
 }
 
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
-                             void* hi, void* lo, cudaStream_t st) {
+                             void* hi, void* lo, cudaStream_t st, int fold) {
+    if (fold && (g.G != 1 || g.S != 1 || chk * CB > WS_CH))
+        return fail(CB_ERR_INVALID, "folded weight pack needs one chunk of an R x 1 kernel");
     if ((int64_t)g.K * kw_pad == 0) return CB_OK;
     if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
         return fail(CB_ERR_MISALIGNED, "packed weights must be 16-byte aligned");
@@ -565,7 +622,7 @@ int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_p
                                              (int)smem);
         if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
     }
-    kern<<<grid, 256, smem, st>>>(g.K, g.cpg, g.R, g.S, CB, chk, kw_pad, w, hi, lo);
+    kern<<<grid, 256, smem, st>>>(g.K, g.cpg, g.R, g.S, CB, chk, kw_pad, w, hi, lo, fold);
     return check_launch("weight_split_taps");
 }
 

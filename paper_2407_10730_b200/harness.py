@@ -128,15 +128,32 @@ def _as_numpy(y) -> np.ndarray:
     return y.cpu().numpy() if hasattr(y, "cpu") else np.asarray(y)
 
 
+def device_inputs(desc: ConvDescriptor, cfg: RunConfig) -> ConvInputs:
+    """Seeded U[-1,1) buffers drawn directly on the GPU (same shapes and distribution as
+    make_inputs, not the same bits).  For large sweeps, where host generation at ~255 MB/s
+    dominates; correctness checks need make_inputs."""
+    import torch
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed((cfg.seed ^ _hash64(key_of(desc))) & 0x7FFFFFFFFFFFFFFF)
+    u = lambda *shape: torch.rand(shape, generator=gen, device="cuda") * 2 - 1
+    x = u(desc.batch, desc.in_channels, desc.in_h, desc.in_w)
+    w = u(desc.out_channels, desc.in_channels // desc.groups, desc.k_h, desc.k_w)
+    b = u(desc.out_channels) if desc.has_bias else None
+    return ConvInputs(desc=desc, input=x, weights=w, bias=b)
+
+
 def run_single(desc: ConvDescriptor, cfg: RunConfig, main_fn: ConvFn | None = None,
                baseline_fn: ConvFn | None = None, ledger_factory=EventLedger,
-               oracle: Callable[[ConvInputs], np.ndarray] | None = None) -> RunOutcome:
+               oracle: Callable[[ConvInputs], np.ndarray] | None = None,
+               inputs_fn: Callable[[ConvDescriptor, RunConfig], ConvInputs] | None = None
+               ) -> RunOutcome:
     """One sweep iteration on the GPU (reference harness.py:107-147).
 
     mode main -> SConv, baseline -> Im2col-GEMM, fused -> fused conv, correctness ->
     main timed, then main vs baseline compared with the reference allclose; when an
     `oracle` is given the outcome's detail also carries the parity metric
-    max|y - oracle| / sqrt(C/g*R*S)."""
+    max|y - oracle| / sqrt(C/g*R*S).  `inputs_fn` replaces host generation + upload
+    (device_inputs); it cannot be combined with an oracle."""
     key = key_of(desc)
     main_fn = main_fn or main_algo(cfg)
     baseline_fn = baseline_fn or baseline_algo(cfg)
@@ -146,8 +163,13 @@ def run_single(desc: ConvDescriptor, cfg: RunConfig, main_fn: ConvFn | None = No
         return RunOutcome(key=key, mode=cfg.mode, runs=cfg.runs, warmups=cfg.warmups,
                           status=status, **kw)
     try:
-        host = make_inputs(desc, cfg)
-        inputs = to_device(host)
+        if inputs_fn is not None:
+            if oracle is not None:
+                raise ValueError("an oracle needs the host inputs of make_inputs")
+            host, inputs = None, inputs_fn(desc, cfg)
+        else:
+            host = make_inputs(desc, cfg)
+            inputs = to_device(host)
         ledger = ledger_factory()
         for _ in range(cfg.warmups):
             ledger.reset()

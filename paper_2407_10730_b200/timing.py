@@ -101,24 +101,31 @@ class PhaseLedger:
 class EventLedger(PhaseLedger):
     """PhaseLedger whose device phases are timed with CUDA events on `stream`.
 
-    start/update only *record* events (asynchronous); snapshot() waits for the last
-    event and converts every pair to integer ns.  Phases in `host_phases` use the host
-    clock exactly like PhaseLedger.
+    start/update only *record* events (asynchronous; raw events through the C ABI,
+    cb_event_record, about 1 us of host time each); snapshot() waits for the last event
+    and converts every pair to integer ns.  Phases in `host_phases` use the host clock
+    exactly like PhaseLedger.  Without an explicit `stream`, events go to the stream that
+    is current at the first record of a run (after reset()); external ledgers resolve it
+    at every record, since they are recorded inside graph captures.
     """
 
     device_timed = True
 
     def __init__(self, stream=None, host_phases: Iterable[Phase] = HOST_PHASES,
                  clock: Callable[[], int] = time.perf_counter_ns, external: bool = False) -> None:
-        import torch  # plumbing only: events + streams
+        import torch  # plumbing only: the current stream
+        from . import _capi
 
         self._torch = torch
+        self._capi = _capi
+        self._lib = _capi.load()
         self._stream = stream
         self._host = frozenset(Phase(p) for p in host_phases)
         # external events may be recorded inside a CUDA-graph capture: the graph then
         # re-records them on every replay, so snapshot() reads the latest replay's times
-        self._external = external
-        self._pool: list = []
+        self._external = 1 if external else 0
+        self._pool: list[int] = []
+        self._st = None
         super().__init__(clock)
 
     def reset(self) -> None:
@@ -127,16 +134,44 @@ class EventLedger(PhaseLedger):
         for pair in getattr(self, "_pairs", []):
             pool.extend(pair[1:])
         self._pool = pool
-        self._pairs: list[tuple[Phase, object, object]] = []
-        self._open_evt: list[object | None] = [None] * len(Phase)
+        self._pairs: list[tuple[Phase, int, int]] = []
+        self._open_evt: list[int | None] = [None] * len(Phase)
+        self._st = None
 
-    def _event(self):
+    def __del__(self) -> None:
+        lib = getattr(self, "_lib", None)
+        if lib is None:
+            return
+        evs = list(getattr(self, "_pool", []))
+        for pair in getattr(self, "_pairs", []):
+            evs.extend(pair[1:])
+        for e in evs:
+            try:
+                lib.cb_event_destroy(e)
+            except Exception:  # interpreter shutdown
+                pass
+
+    def _event(self) -> int:
         if self._pool:
             return self._pool.pop()
-        return self._torch.cuda.Event(enable_timing=True, external=self._external)
+        import ctypes
+        h = ctypes.c_void_p()
+        self._capi.check(self._lib.cb_event_create(ctypes.byref(h)))
+        return h.value
 
-    def _cur_stream(self):
-        return self._stream if self._stream is not None else self._torch.cuda.current_stream()
+    def _stream_handle(self) -> int:
+        if self._st is None or self._external:
+            s = self._stream if self._stream is not None else self._torch.cuda.current_stream()
+            st = getattr(s, "cuda_stream", s)
+            if self._external:
+                return st
+            self._st = st
+        return self._st
+
+    def _record(self) -> int:
+        ev = self._event()
+        self._capi.check(self._lib.cb_event_record(ev, self._stream_handle(), self._external))
+        return ev
 
     def start(self, phase: Phase) -> None:
         phase = Phase(phase)
@@ -144,9 +179,7 @@ class EventLedger(PhaseLedger):
             return super().start(phase)
         if self._open_evt[phase] is not None:
             raise TimingStateError(f"start({phase.name}) while already started")
-        ev = self._event()
-        ev.record(self._cur_stream())
-        self._open_evt[phase] = ev
+        self._open_evt[phase] = self._record()
 
     def update(self, phase: Phase) -> None:
         phase = Phase(phase)
@@ -155,24 +188,23 @@ class EventLedger(PhaseLedger):
         ev0 = self._open_evt[phase]
         if ev0 is None:
             raise TimingStateError(f"update({phase.name}) without a matching start")
-        ev1 = self._event()
-        ev1.record(self._cur_stream())
+        ev1 = self._record()
         self._pairs.append((phase, ev0, ev1))
         self._open_evt[phase] = None
 
     def snapshot(self) -> TimingReport:
+        import ctypes
         open_ = [p.name for p in Phase
                  if self._pending[p] is not None or self._open_evt[p] is not None]
         if open_:
             raise TimingStateError(f"snapshot with pending starts: {', '.join(open_)}")
         elapsed = list(self._elapsed)
         calls = list(self._calls)
-        if self._pairs:
-            self._pairs[-1][2].synchronize()
-            for phase, e0, e1 in self._pairs:
-                e1.synchronize()
-                elapsed[phase] += int(round(e0.elapsed_time(e1) * 1e6))
-                calls[phase] += 1
+        ns = ctypes.c_int64()
+        for phase, e0, e1 in self._pairs:
+            self._capi.check(self._lib.cb_event_elapsed_ns(e0, e1, ctypes.byref(ns)))
+            elapsed[phase] += ns.value
+            calls[phase] += 1
         return _report(elapsed, calls)
 
 

@@ -1,0 +1,66 @@
+"""Results-CSV schema (reference report.py:21-27) and the config-5 sweep plumbing (CPU)."""
+
+from __future__ import annotations
+
+import csv
+import importlib.util
+from pathlib import Path
+
+from paper_2407_10730_b200 import configs, report
+from paper_2407_10730_b200.harness import RunOutcome
+from paper_2407_10730_b200.timing import TimingReport, aggregate, Phase
+
+ROOT = Path(__file__).resolve().parent.parent
+STEMS = ["pre_analysis", "pre_reorder", "in_tiling", "in_packing", "in_microkernel",
+         "in_unpacking", "post_reorder"]
+
+
+def _sweep_mod():
+    spec = importlib.util.spec_from_file_location("sweep_tool", ROOT / "tools" / "sweep.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_results_header_is_reference_schema():
+    want = ["key", "mode", "status", "runs", "warmups"]
+    for s in STEMS:
+        want += [f"{s}_ns_mean", f"{s}_ns_min", f"{s}_calls"]
+    want += ["operation_ns_mean", "operation_ns_min", "convolution_ns_mean",
+             "convolution_ns_min", "correctness_max_rel_err"]
+    assert report.RESULTS_HEADER == want
+
+
+def _report(vals):
+    from paper_2407_10730_b200.timing import _report as mk
+    return mk(vals, [1 if v else 0 for v in vals])
+
+
+def test_results_roundtrip(tmp_path):
+    stats = aggregate([_report([0, 100, 0, 0, 400, 0, 0]), _report([0, 120, 0, 0, 380, 0, 0])])
+    outs = [RunOutcome(key="k1", mode="baseline", runs=2, warmups=1, status="ok", stats=stats),
+            RunOutcome(key="k2", mode="baseline", runs=2, warmups=1,
+                       status="skipped_unsupported", detail="groups")]
+    p = tmp_path / "r.csv"
+    report.write_results_csv(outs, p)
+    rows = report.read_results_csv(p)
+    assert [r.key for r in rows] == ["k1", "k2"]
+    assert rows[0].operation_ns_mean == 500.0 and rows[0].operation_ns_min == 480
+    assert rows[0].phase_ns_mean[Phase.PRE_REORDER] == 110.0
+    assert rows[1].operation_ns_mean is None
+    with open(p) as fh:
+        assert len(next(csv.reader(fh))) == len(report.RESULTS_HEADER)
+
+
+def test_stratified_sample_and_lpt_cover_the_sweep():
+    sw = _sweep_mod()
+    descs = configs.sweep(500, 0)
+    a = sw.stratified_sample(descs, 50, 0)
+    assert a == sw.stratified_sample(descs, 50, 0) and len(a) == 50 == len(set(a))
+    from paper_2407_10730_b200.shard import lpt_assign
+    peaks = {"hbm_gbs": 6500.0, "bf16_tflops": 1600.0, "bf16_tflops_sustained": 1400.0}
+    cost = [sw.predicted_s(descs[i], peaks) for i in a]
+    parts = lpt_assign(cost, 4)
+    assert sorted(j for p in parts for j in p) == list(range(len(a)))
+    loads = [sum(cost[j] for j in p) for p in parts]
+    assert max(loads) <= sum(loads) / 4 + max(cost) + 1e-12

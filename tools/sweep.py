@@ -1,0 +1,177 @@
+"""BASELINE.json config 5: the synthetic convSet sweep on N GPUs.
+
+    python tools/sweep.py --sample 400 --modes fused,baseline,main --out sweep_out
+    torchrun --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29501 \
+        tools/sweep.py --out sweep_out
+
+Ops are independent, so ranks split them by LPT on the predicted roofline time (no
+collective on the data path; gloo carries only the barrier and the final gather).  Every
+rank runs its ops through the package harness (run_single: warmups, then measured runs on
+a CUDA-event ledger), one mode after another.  Rank 0 writes
+
+  <out>/results_<mode>.csv   reference results schema (report.py:21-27), sweep order
+  <out>/summary.json         per mode: GFLOP/s p10/p50/p90, roofline-fraction
+                             distribution, pack share of the stepwise paths, status
+                             counts, per-rank device-time makespan and the aggregate
+                             GFLOP/s it implies
+
+--sample K keeps a seeded, FLOP-stratified subset of K ops (the full 9243-op sweep needs
+~13 min of host input generation per process; --device-inputs draws the same
+distribution on the GPU instead, which is not bit-identical to make_inputs).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np
+
+from paper_2407_10730_b200 import algos, configs, harness, report, roofline
+from paper_2407_10730_b200.descriptor import flop_count
+from paper_2407_10730_b200.shard import lpt_assign
+from paper_2407_10730_b200.timing import Phase
+
+LAUNCH_FLOOR_S = 5e-6  # per-op floor added to the roofline for LPT balance
+
+
+def stratified_sample(descs, k: int, seed: int) -> list[int]:
+    """k indices spread evenly over the FLOP-sorted sweep (seeded pick inside each stratum)."""
+    if k >= len(descs):
+        return list(range(len(descs)))
+    order = sorted(range(len(descs)), key=lambda i: flop_count(descs[i]))
+    rng = random.Random(seed)
+    edges = np.linspace(0, len(order), k + 1).astype(int)
+    return sorted(order[rng.randrange(a, b)] for a, b in zip(edges[:-1], edges[1:]) if b > a)
+
+
+def predicted_s(desc, peaks) -> float:
+    return roofline.conv_roofline(desc, algos.FUSED_DEFAULT_VARIANT, peaks)["t_roofline_s"] + LAUNCH_FLOOR_S
+
+
+def pack_share(o, mode: str) -> float | None:
+    if o.stats is None or not o.stats.operation_ns_mean:
+        return None
+    m = o.stats.phase_ns_mean
+    pack = m[Phase.IN_PACKING] + (m[Phase.PRE_REORDER] if mode == "baseline" else 0.0)
+    return pack / o.stats.operation_ns_mean
+
+
+def pct(vals, q):
+    return float(np.percentile(vals, q)) if vals else None
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--ops", type=int, default=configs.SWEEP_SIZE)
+    ap.add_argument("--seed", type=int, default=0, help="sweep generator seed")
+    ap.add_argument("--data-seed", type=int, default=0, help="make_inputs seed")
+    ap.add_argument("--sample", type=int, default=0, help="stratified subset size (0: all)")
+    ap.add_argument("--modes", default="fused,baseline,main")
+    ap.add_argument("--warmups", type=int, default=3)
+    ap.add_argument("--runs", type=int, default=10)
+    ap.add_argument("--variant", default=None, help="stepwise variant (default tc3xtf32)")
+    ap.add_argument("--fused-variant", default=algos.FUSED_DEFAULT_VARIANT)
+    ap.add_argument("--device-inputs", action="store_true")
+    ap.add_argument("--max-gflop", type=float, default=0.0, help="skip larger ops (0: none)")
+    ap.add_argument("--out", default="sweep_out")
+    args = ap.parse_args(argv)
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+
+    descs = configs.sweep(args.ops, args.seed)
+    idx = stratified_sample(descs, args.sample, args.seed) if args.sample else list(range(len(descs)))
+    if args.max_gflop > 0:
+        idx = [i for i in idx if flop_count(descs[i]) <= args.max_gflop * 1e9]
+    peaks = roofline.load_peaks()
+    cost = [predicted_s(descs[i], peaks) for i in idx]
+    mine = [idx[j] for j in lpt_assign(cost, world)[rank]]
+    modes = [m for m in args.modes.split(",") if m]
+    inputs_fn = harness.device_inputs if args.device_inputs else None
+
+    local_rows: dict[str, list] = {m: [] for m in modes}
+    busy = {m: 0.0 for m in modes}
+    t0 = time.time()
+    for m in modes:
+        variant = args.fused_variant if m == "fused" else (args.variant or algos.DEFAULT_VARIANT)
+        cfg = harness.RunConfig(mode=m, warmups=args.warmups, runs=args.runs,
+                                seed=args.data_seed, variant=variant)
+        for n, i in enumerate(mine):
+            o = harness.run_single(descs[i], cfg, inputs_fn=inputs_fn)
+            rf = roofline.conv_roofline(descs[i], variant, peaks)
+            t_op = o.stats.operation_ns_mean * 1e-9 if o.stats else None
+            if t_op:
+                busy[m] += t_op
+            local_rows[m].append({
+                "index": i, "record": report.outcome_record(o), "status": o.status,
+                "flops": rf["flops"], "t_s": t_op,
+                "t_min_s": o.stats.operation_ns_min * 1e-9 if o.stats else None,
+                "roofline_s": rf["t_roofline_s"], "pack_share": pack_share(o, m),
+                "detail": o.detail})
+            if rank == 0 and (n + 1) % 100 == 0:
+                print(f"[rank0] {m}: {n + 1}/{len(mine)} ops, {time.time() - t0:.0f} s", flush=True)
+            del o
+        torch.cuda.empty_cache()
+
+    gathered = [None] * world
+    payload = {"rows": local_rows, "busy": busy, "n": len(mine)}
+    if dist is not None:
+        dist.all_gather_object(gathered, payload)
+    else:
+        gathered = [payload]
+    if rank == 0:
+        out = Path(args.out)
+        out.mkdir(parents=True, exist_ok=True)
+        summary = {"ops_total": len(descs), "ops_run": len(idx), "sweep_seed": args.seed,
+                   "data_seed": args.data_seed, "sample": args.sample, "world": world,
+                   "inputs": "device (torch.rand, not make_inputs bits)" if args.device_inputs
+                   else "make_inputs (bit-identical to the reference)",
+                   "warmups": args.warmups, "runs": args.runs, "peaks": peaks, "modes": {}}
+        for m in modes:
+            rows = sorted((r for g in gathered for r in g["rows"][m]), key=lambda r: r["index"])
+            report.write_results_csv([r["record"] for r in rows], out / f"results_{m}.csv")
+            ok = [r for r in rows if r["status"] == "ok" and r["t_s"]]
+            gfs = [r["flops"] / r["t_s"] / 1e9 for r in ok]
+            frac = [r["roofline_s"] / r["t_s"] for r in ok]
+            shares = [r["pack_share"] for r in ok if r["pack_share"] is not None]
+            makespan = max(g["busy"][m] for g in gathered)
+            flops = sum(r["flops"] for r in ok)
+            summary["modes"][m] = {
+                "variant": args.fused_variant if m == "fused" else (args.variant or algos.DEFAULT_VARIANT),
+                "status": {s: sum(r["status"] == s for r in rows) for s in
+                           ("ok", "skipped_unsupported", "failed")},
+                "gflops_p10_p50_p90": [pct(gfs, 10), pct(gfs, 50), pct(gfs, 90)],
+                "roofline_frac_p10_p50_p90": [pct(frac, 10), pct(frac, 50), pct(frac, 90)],
+                "pack_share_p10_p50_p90": [pct(shares, 10), pct(shares, 50), pct(shares, 90)]
+                if m != "fused" else None,
+                "total_tflop": flops / 1e12,
+                "device_makespan_s": makespan,
+                "aggregate_tflops": flops / makespan / 1e12 if makespan else None,
+                "per_rank_busy_s": [g["busy"][m] for g in gathered],
+                "failed": [(r["index"], r["detail"]) for r in rows if r["status"] == "failed"][:20],
+            }
+        (out / "summary.json").write_text(json.dumps(summary, indent=1) + "\n")
+        print(json.dumps({m: {k: v for k, v in s.items() if k != "failed"}
+                          for m, s in summary["modes"].items()}, indent=1))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
