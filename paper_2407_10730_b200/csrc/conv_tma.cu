@@ -208,44 +208,49 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
 
     if (warp == PRODUCER_WARP) {
         // ================================ TMA producer ==================================
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            constexpr uint32_t tx = CG * (2 * Cfg::A_BYTES + 2 * Cfg::B_BYTES);
-            for (int64_t t = cl0; t < p.total_items; t += ncl) {
-                const WorkItem it = decode_item(p, t);
-                const int gi = it.gi;
-                const int64_t m0 = it.mt * (TMA_BM * CG) + rank * TMA_BM;
-                const int n0 = (int)(m0 / g.PQ);
-                const int rem = (int)(m0 - (int64_t)n0 * g.PQ);
-                const int oy0 = rem / g.Q, ox0 = rem - (rem / g.Q) * g.Q;
-                const int wc = ox0 * g.sw - g.pw, hc = oy0 * g.sh - g.ph;
-                const int brow = gi * g.kpg + it.nt * BN + (int)rank * Cfg::B_ROWS;
-                for (int kb = it.kb0; kb < it.kb1; ++kb) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
-                    if (p.debug & 1) {  // diagnostics: MMA-only timing, no operand traffic
-                        if (rank == 0) ptx::mbar_arrive(&full[stage]);
-                        if (++stage == STAGES) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                        continue;
+        // The whole warp walks the schedule (warp-uniform values in uniform registers);
+        // one elected lane issues.  The (tap, chunk) walk advances by counters.
+        const uint32_t leader = ptx::elect_one();
+        int stage = 0;
+        uint32_t phase = 0;
+        constexpr uint32_t tx = CG * (2 * Cfg::A_BYTES + 2 * Cfg::B_BYTES);
+        for (int64_t t = cl0; t < p.total_items; t += ncl) {
+            const WorkItem it = decode_item(p, t);
+            const int gi = it.gi;
+            const int64_t m0 = it.mt * (TMA_BM * CG) + rank * TMA_BM;
+            const int n0 = (int)(m0 / g.PQ);
+            const int rem = (int)(m0 - (int64_t)n0 * g.PQ);
+            const int oy0 = rem / g.Q, ox0 = rem - (rem / g.Q) * g.Q;
+            const int wc = ox0 * g.sw - g.pw, hc = oy0 * g.sh - g.ph;
+            const int brow = gi * g.kpg + it.nt * BN + (int)rank * Cfg::B_ROWS;
+            int q = it.kb0 * L.cps;  // chunk index = (r*S + s)*chk + cbi
+            int tap = q / L.chk;
+            int cbi = q - tap * L.chk;
+            int r = tap / g.S;
+            int s = tap - r * g.S;
+            for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+                if (p.debug & 1) {  // diagnostics: MMA-only timing, no operand traffic
+                    if (leader && rank == 0) ptx::mbar_arrive(&full[stage]);
+                    __syncwarp();
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
                     }
-                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], tx);
-                    const uint32_t lbar = ptx::leader_bar(&full[stage]);
-                    for (int i = 0; i < L.cps; ++i) {
-                        const int q = kb * L.cps + i;
-                        int c = L.c_alloc, offw = 0, offh = 0;  // past the end: all-OOB zeros
-                        if (q < L.total_chunks) {
-                            const int tap = q / L.chk;
-                            const int cbi = q - tap * L.chk;
-                            const int r = tap / g.S, s = tap - (tap / g.S) * g.S;
-                            c = gi * g.cpg + cbi * L.cb;
-                            offw = s * g.dw;
-                            offh = r * g.dh;
-                        }
-                        const int off = i * TMA_BM * L.chunk_bytes;
+                    continue;
+                }
+                if (leader && rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], tx);
+                const uint32_t lbar = ptx::leader_bar(&full[stage]);
+                for (int i = 0; i < L.cps; ++i, ++q) {
+                    int c = L.c_alloc, offw = 0, offh = 0;  // past the end: all-OOB zeros
+                    if (q < L.total_chunks) {
+                        c = gi * g.cpg + cbi * L.cb;
+                        offw = s * g.dw;
+                        offh = r * g.dh;
+                    }
+                    const int off = i * TMA_BM * L.chunk_bytes;
+                    if (leader) {
                         if (CG == 2) {
                             ptx::tma_load_im2col_4d_pair(st + off, &tm_ahi, lbar, c, wc, hc, n0,
                                                          (uint16_t)offw, (uint16_t)offh);
@@ -258,7 +263,16 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                                                     c, wc, hc, n0, (uint16_t)offw, (uint16_t)offh);
                         }
                     }
-                    uint8_t* bdst = st + 2 * Cfg::A_BYTES;
+                    if (++cbi == L.chk) {
+                        cbi = 0;
+                        if (++s == g.S) {
+                            s = 0;
+                            ++r;
+                        }
+                    }
+                }
+                uint8_t* bdst = st + 2 * Cfg::A_BYTES;
+                if (leader) {
                     if (CG == 2) {
                         ptx::tma_load_2d_pair(bdst, &tm_bhi, lbar, kb * Cfg::KE, brow);
                         ptx::tma_load_2d_pair(bdst + Cfg::B_BYTES, &tm_blo, lbar, kb * Cfg::KE, brow);
@@ -267,17 +281,30 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                         ptx::tma_load_2d(bdst + Cfg::B_BYTES, &tm_blo, &full[stage], kb * Cfg::KE,
                                          brow);
                     }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
     } else if (warp == MMA_WARP) {
-        // ============================ MMA issuer (leader) ===============================
-        if (lane == 0 && rank == 0) {
+        // ============================ MMA issuer (leader CTA) =============================
+        // Whole warp walks the schedule; descriptors are the stage-0 descriptors plus
+        // constant offsets (the 14-bit address field never carries inside smem); one
+        // elected lane issues the 12 MMAs of a K block and the commits.
+        if (rank == 0) {
             constexpr uint32_t idesc = ptx::idesc_f32acc<BF16>(TMA_BM * CG, BN);
+            constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4;
+            constexpr uint32_t ALO16 = Cfg::A_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
+            const uint32_t s0 = ptx::smem_u32(smem);
+            const uint64_t da0 = a_desc(s0, L.chunk_bytes, 0);
+            uint32_t aoff[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) aoff[kk] = (uint32_t)(a_desc(s0, L.chunk_bytes, kk) - da0);
+            const uint64_t db0 = ptx::sdesc_k_sw128(s0 + 2 * Cfg::A_BYTES);
+            const uint32_t leader = ptx::elect_one();
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -288,44 +315,47 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                const int kb0 = it.kb0;
                 for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
-                    const uint32_t a_hi = ptx::smem_u32(smem + stage * Cfg::STAGE_BYTES);
-                    const uint32_t a_lo = a_hi + Cfg::A_BYTES;
-                    const uint32_t b_hi = a_hi + 2 * Cfg::A_BYTES;
-                    const uint32_t b_lo = b_hi + Cfg::B_BYTES;
+                    const uint64_t sa = da0 + (uint64_t)(stage * STG16);
+                    const uint64_t sb = db0 + (uint64_t)(stage * STG16);
+                    if (leader) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t dah = a_desc(a_hi, L.chunk_bytes, kk);
-                        const uint64_t dal = a_desc(a_lo, L.chunk_bytes, kk);
-                        const uint64_t dbh = ptx::sdesc_k_sw128(b_hi + kk * 32);
-                        const uint64_t dbl = ptx::sdesc_k_sw128(b_lo + kk * 32);
-                        const uint32_t first = (kb != kb0 || kk != 0) ? 1u : 0u;
-                        if (CG == 2) {
-                            ptx::umma_pair<BF16>(d, dal, dbh, idesc, first);
-                            ptx::umma_pair<BF16>(d, dah, dbl, idesc, 1);
-                            ptx::umma_pair<BF16>(d, dah, dbh, idesc, 1);
-                        } else {
-                            ptx::umma<BF16>(d, dal, dbh, idesc, first);
-                            ptx::umma<BF16>(d, dah, dbl, idesc, 1);
-                            ptx::umma<BF16>(d, dah, dbh, idesc, 1);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t dah = sa + aoff[kk];
+                            const uint64_t dal = dah + ALO16;
+                            const uint64_t dbh = sb + 2 * kk;
+                            const uint64_t dbl = dbh + BLO16;
+                            const uint32_t first = (kb != it.kb0 || kk != 0) ? 1u : 0u;
+                            if (CG == 2) {
+                                ptx::umma_pair<BF16>(d, dal, dbh, idesc, first);
+                                ptx::umma_pair<BF16>(d, dah, dbl, idesc, 1);
+                                ptx::umma_pair<BF16>(d, dah, dbh, idesc, 1);
+                            } else {
+                                ptx::umma<BF16>(d, dal, dbh, idesc, first);
+                                ptx::umma<BF16>(d, dah, dbl, idesc, 1);
+                                ptx::umma<BF16>(d, dah, dbh, idesc, 1);
+                            }
                         }
+                        if (CG == 2)
+                            ptx::umma_commit_pair(&empty[stage]);
+                        else
+                            ptx::umma_commit(&empty[stage]);
                     }
-                    if (CG == 2)
-                        ptx::umma_commit_pair(&empty[stage]);
-                    else
-                        ptx::umma_commit(&empty[stage]);
+                    __syncwarp();
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if (CG == 2)
-                    ptx::umma_commit_pair(&tfull[acc]);
-                else
-                    ptx::umma_commit(&tfull[acc]);
+                if (leader) {
+                    if (CG == 2)
+                        ptx::umma_commit_pair(&tfull[acc]);
+                    else
+                        ptx::umma_commit(&tfull[acc]);
+                }
+                __syncwarp();
             }
         }
     } else {

@@ -149,6 +149,17 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// One lane of a converged warp (elect.sync): the issuing lane of warp-uniform loops, so
+// operands computed by the whole warp stay in uniform registers (no per-instruction
+// waterfall of R2UR.BROADCAST loops around each tcgen05 / TMA instruction).
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred;
+}
+
 // ---- tcgen05: MMA ----------------------------------------------------------------------
 // D[tmem] (+)= A[smem] * B[smem]^T, A: M x K, B: N x K, both K-major.
 template <bool BF16>

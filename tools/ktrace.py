@@ -47,7 +47,7 @@ def main(name="cfg4", variant="tc3xbf16"):
     starts = rel[:, 0]
     ends = rel[:, -1]
     print(f"  epilogue-ready  min {np.nanmin(starts):7.1f} max {np.nanmax(starts):7.1f} us")
-    for k in range(1, 8):
+    for k in range(1, 13):
         col = rel[:, k]
         if np.all(np.isnan(col)):
             break
