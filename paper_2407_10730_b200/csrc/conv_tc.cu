@@ -248,57 +248,67 @@ conv_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ CUten
         }
     } else if (warp == 4) {
         // ============================ weight TMA producer =============================
-        if (lane == 0) {
-            const int row0 = gi * g.kpg + tile_n * BN;
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int i = 0; i < nkb; ++i) {
-                ptx::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+        // converged warp, one elected lane issues (operands stay in uniform registers)
+        const uint32_t leader = ptx::elect_one();
+        const int row0 = gi * g.kpg + tile_n * BN;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int i = 0; i < nkb; ++i) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+            const int kc = (kb_begin + i) * BK;
+            if (leader) {
                 ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::B_BYTES);
-                const int kc = (kb_begin + i) * BK;
                 ptx::tma_load_2d(st + 2 * Cfg::A_BYTES, &tm_hi, &full[stage], kc, row0);
                 ptx::tma_load_2d(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tm_lo, &full[stage], kc,
                                  row0);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
             }
         }
     } else {
         // ============================== MMA issuer ====================================
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_f32acc<BF16>(TC_BM, BN);
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int i = 0; i < nkb; ++i) {
-                ptx::mbar_wait(&full[stage], phase);
-                ptx::tc_fence_after();
-                const uint32_t a_hi = ptx::smem_u32(smem + stage * Cfg::STAGE_BYTES);
-                const uint32_t a_lo = a_hi + Cfg::A_BYTES;
-                const uint32_t b_hi = a_hi + 2 * Cfg::A_BYTES;
-                const uint32_t b_lo = b_hi + Cfg::B_BYTES;
+        // converged warp; descriptors = stage-0 descriptors + constant offsets; one elected
+        // lane issues
+        constexpr uint32_t idesc = ptx::idesc_f32acc<BF16>(TC_BM, BN);
+        constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4;
+        constexpr uint32_t ALO16 = Cfg::A_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
+        const uint32_t s0 = ptx::smem_u32(smem);
+        const uint64_t da0 = ptx::sdesc_k_sw128(s0);
+        const uint64_t db0 = ptx::sdesc_k_sw128(s0 + 2 * Cfg::A_BYTES);
+        const uint32_t leader = ptx::elect_one();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int i = 0; i < nkb; ++i) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint64_t sa = da0 + (uint64_t)(stage * STG16);
+            const uint64_t sb = db0 + (uint64_t)(stage * STG16);
+            if (leader) {
 #pragma unroll
                 for (int kk = 0; kk < BK / Cfg::UK; ++kk) {
-                    const uint32_t koff = kk * 32;  // bytes along the swizzled row
-                    const uint64_t dah = ptx::sdesc_k_sw128(a_hi + koff);
-                    const uint64_t dal = ptx::sdesc_k_sw128(a_lo + koff);
-                    const uint64_t dbh = ptx::sdesc_k_sw128(b_hi + koff);
-                    const uint64_t dbl = ptx::sdesc_k_sw128(b_lo + koff);
+                    const uint64_t dah = sa + 2 * kk;  // 32 bytes along the swizzled row
+                    const uint64_t dal = dah + ALO16;
+                    const uint64_t dbh = sb + 2 * kk;
+                    const uint64_t dbl = dbh + BLO16;
                     // small terms first, then the dominant hi*hi product
                     ptx::umma<BF16>(tmem_base, dal, dbh, idesc, (i | kk) != 0);
                     ptx::umma<BF16>(tmem_base, dah, dbl, idesc, 1);
                     ptx::umma<BF16>(tmem_base, dah, dbh, idesc, 1);
                 }
                 ptx::umma_commit(&empty[stage]);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
             }
-            ptx::umma_commit(tmem_full);
+            __syncwarp();
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
         }
+        if (leader) ptx::umma_commit(tmem_full);
+        __syncwarp();
     }
 
     ptx::tc_fence_before();

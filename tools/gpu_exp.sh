@@ -1,3 +1,4 @@
 set -o pipefail
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -2
-timeout 300 python tools/ktime.py pack cfg1 cfg2a cfg2b cfg3 cfg4 2>&1 | tail -10
+timeout 240 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+timeout 200 python tools/phase_probe.py n1_c256x14x14_f256x3x3_s1x1_p1x1_d1x1_g1_b0 2>&1 | tail -3
+timeout 200 python tools/devtime.py cfg4 2>&1 | tail -12
