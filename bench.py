@@ -300,17 +300,20 @@ def run_ours(args):
     x_p = torch.from_numpy(x_h).pin_memory()
     w_p = torch.from_numpy(w_h).pin_memory()
     y_p = torch.empty(ys[0].shape, dtype=torch.float32).pin_memory()
-    inp_h = algos.ConvInputs(desc=d, input=x_p, weights=w_p)
+    # HostPipeline: the package's host-buffer API -- per step, x and w go host->device and
+    # y device->host, on their own streams, overlapping the neighbouring steps' kernels
+    pipe = algos.HostPipeline(d, variant)
     for _ in range(max(1, args.warmup)):
-        algos.conv_fused(inp_h, variant=variant, workspace=fc.workspace, out=y_p)
-    torch.cuda.synchronize()
+        pipe.submit(x_p, w_p, y_p)
+    pipe.synchronize()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
+    pipe.wait_streams_for(e0)
     for _ in range(args.steps):
-        algos.conv_fused(inp_h, variant=variant, workspace=fc.workspace, out=y_p)
-    e1.record()
+        pipe.submit(x_p, w_p, y_p)
+    pipe.record_done(e1)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
     if dist is not None:
@@ -318,6 +321,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+           "api": "HostPipeline.submit (pinned host x, w in; y out; copies overlap kernels)",
            "h2d_bytes_per_step": int(x_h.nbytes + w_h.nbytes),
            "d2h_bytes_per_step": int(y_p.numel() * 4)}
 

@@ -6,7 +6,7 @@ libconvb200.so (include/convb200.h), with the paper's per-step timing nomenclatu
 Importing needs no GPU; calling an algorithm does (there is no CPU fallback).
 """
 
-from .algos import (DEFAULT_VARIANT, CacheParams, ConvInputs, GemmBlocking,
+from .algos import (DEFAULT_VARIANT, CacheParams, ConvInputs, FusedConv, GemmBlocking, HostPipeline,
                     UnsupportedDescriptorError, conv_baseline_im2col_gemm, conv_fused,
                     conv_main_blocked_direct, gemm, im2col_transform, plan_sconv, plan_tiles,
                     split_weights)

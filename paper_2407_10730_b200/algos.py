@@ -655,3 +655,76 @@ class FusedConv:
         with torch.cuda.graph(graph):
             self.run(x_dev, y_dev, bias_dev, ledger=ledger, weights=w_dev)
         return graph
+
+
+class HostPipeline:
+    """Fused convolutions on HOST buffers, streamed: three CUDA streams (host->device copy,
+    compute, device->host copy) and `depth` device buffer sets, ordered by events, so step
+    i's input upload overlaps step i-1's kernels and step i-2's result download.
+
+    Every submit() copies that step's x (and w) from the caller's host buffers and its
+    y back into the caller's host buffer -- the same work as conv_fused(host inputs), with
+    the transfers in flight concurrently instead of back to back.  Pinned host buffers make
+    the copies asynchronous.  synchronize() waits for every submitted step."""
+
+    def __init__(self, desc, variant: str = FUSED_DEFAULT_VARIANT, depth: int = 2,
+                 device="cuda"):
+        torch = _torch()
+        self.desc = desc
+        self.fc = FusedConv(desc, variant, device)
+        dev = self.fc.device
+        self.depth = depth
+        d = desc
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.comp = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        mk = lambda shape: torch.empty(shape, dtype=torch.float32, device=dev)
+        self.x = [mk((d.batch, d.in_channels, d.in_h, d.in_w)) for _ in range(depth)]
+        self.w = [mk((d.out_channels, d.in_channels // d.groups, d.k_h, d.k_w))
+                  for _ in range(depth)]
+        self.y = [mk(self.fc.out_shape) for _ in range(depth)]
+        self.b = [mk((d.out_channels,)) if d.has_bias else None for _ in range(depth)]
+        ev = lambda: torch.cuda.Event()
+        self.uploaded = [ev() for _ in range(depth)]
+        self.computed = [ev() for _ in range(depth)]
+        self.downloaded = [ev() for _ in range(depth)]
+        self.i = 0
+
+    def submit(self, x_host, w_host, y_host, bias_host=None) -> None:
+        torch = _torch()
+        s = self.i % self.depth
+        if self.i >= self.depth:  # slot s was last used by step i - depth
+            self.h2d.wait_event(self.computed[s])       # its x / w consumed
+            self.comp.wait_event(self.downloaded[s])    # its y copied out
+        with torch.cuda.stream(self.h2d):
+            self.x[s].copy_(x_host, non_blocking=True)
+            self.w[s].copy_(w_host, non_blocking=True)
+            if self.b[s] is not None:
+                self.b[s].copy_(bias_host, non_blocking=True)
+            self.uploaded[s].record(self.h2d)
+        self.comp.wait_event(self.uploaded[s])
+        with torch.cuda.stream(self.comp):
+            self.fc.run(self.x[s], self.y[s], self.b[s], weights=self.w[s])
+            self.computed[s].record(self.comp)
+        self.d2h.wait_event(self.computed[s])
+        with torch.cuda.stream(self.d2h):
+            y_host.copy_(self.y[s], non_blocking=True)
+            self.downloaded[s].record(self.d2h)
+        self.i += 1
+
+    def wait_streams_for(self, event) -> None:
+        """Order all three streams after `event` (e.g. a timing start event)."""
+        for st in (self.h2d, self.comp, self.d2h):
+            st.wait_event(event)
+
+    def record_done(self, event) -> None:
+        """Record `event` after every submitted step (all three streams)."""
+        torch = _torch()
+        cur = torch.cuda.current_stream()
+        for st in (self.h2d, self.comp, self.d2h):
+            cur.wait_stream(st)
+        event.record(cur)
+
+    def synchronize(self) -> None:
+        for st in (self.h2d, self.comp, self.d2h):
+            st.synchronize()

@@ -202,3 +202,25 @@ def test_known_answers(cuda):
         assert (fn(inp, PhaseLedger()) == 9.5).all()
     for v in VARIANTS:
         assert (conv_fused(inp, variant=v) == 9.5).all()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2a"])
+def test_host_pipeline_matches_dropin(cuda, name):
+    """HostPipeline (streamed host buffers) gives the drop-in's bits, step after step, and
+    matches the oracle."""
+    import torch
+    from paper_2407_10730_b200.algos import HostPipeline, conv_fused
+    d = cfg(name)
+    inp, (x, w, b) = _inputs(d)
+    want = conv_fused(inp)
+    pipe = HostPipeline(d)
+    xs = [torch.from_numpy(x).pin_memory(), torch.from_numpy(x[:, ::-1].copy()).pin_memory()]
+    wp = torch.from_numpy(w).pin_memory()
+    ys = [torch.empty(want.shape, dtype=torch.float32).pin_memory() for _ in range(3)]
+    for i in range(3):  # more steps than buffer slots: slot reuse is ordered by events
+        pipe.submit(xs[i % 2], wp, ys[i])
+    pipe.synchronize()
+    assert np.array_equal(ys[0].numpy(), want) and np.array_equal(ys[2].numpy(), want)
+    flipped = conv_fused(_inputs(d)[0].__class__(desc=d, input=x[:, ::-1].copy(), weights=w))
+    assert np.array_equal(ys[1].numpy(), flipped)
+    _check_conv(d, ys[0].numpy(), orc.conv_direct_naive(d, x, w, b))
