@@ -625,8 +625,22 @@ class FusedConv:
         """One step on device buffers: [K3 if `weights` is given] -> K0 -> K6.  Without a
         ledger nothing is timed and nothing synchronises (safe under graph capture)."""
         ledger = ledger if ledger is not None else _NULL_LEDGER
-        st = _stream()
-        if weights is not None:
+        torch = _torch()
+        cur = torch.cuda.current_stream()
+        st = cur.cuda_stream
+        # Untimed steps fork K3 (weights) onto a side stream so it overlaps K0 (activations);
+        # K6 joins both.  Timed steps run serially so each phase's events bracket one kernel.
+        fork = weights is not None and ledger is _NULL_LEDGER and self.workspace is not None
+        if fork:
+            if not hasattr(self, "_side"):
+                self._side = torch.cuda.Stream(device=self.device)
+                self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
+            self._ev_fork.record(cur)
+            self._side.wait_event(self._ev_fork)
+            with torch.cuda.stream(self._side):
+                self.pack_weights(weights)
+                self._ev_join.record(self._side)
+        elif weights is not None:
             with _phase(ledger, Phase.PRE_REORDER):
                 self.pack_weights(weights)
         ws = self.workspace.data_ptr() if self.workspace is not None else None
@@ -634,6 +648,8 @@ class FusedConv:
             with _phase(ledger, Phase.IN_PACKING):
                 _capi.check(self._lib.cb_fused_pack_input(self.vid, ctypes.byref(self._cd),
                                                           x_dev.data_ptr(), ws, self.ws_bytes, st))
+        if fork:
+            cur.wait_event(self._ev_join)
         with _phase(ledger, Phase.IN_MICROKERNEL):
             _capi.check(self._lib.cb_conv_fused_packed(
                 self.vid, ctypes.byref(self._cd), x_dev.data_ptr(), ws, self.ws_bytes,
