@@ -33,17 +33,32 @@ KEYS = [
 ]
 
 
-def raw_metrics(rep: Path) -> dict:
+SHORT = {"conv_tma_kernel": "conv_tma", "act_split_nhwc_kernel": "act_split",
+         "act_fold_split_kernel": "act_fold_split", "weight_split_taps_kernel": "weight_split_taps",
+         "im2col_band_kernel": "im2col_band", "im2col_kernel": "im2col_kernel",
+         "conv_tc_kernel": "conv_tc"}
+
+
+def raw_metrics(rep: Path) -> list[dict]:
+    """One dict per profiled kernel launch in the report."""
     out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    res = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""}
-    for k in KEYS:
-        if k in hdr:
-            i = hdr.index(k)
-            res[k] = (vals[i], units[i])
+    hdr, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        m = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""}
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                m[k] = (vals[i], units[i])
+        res.append(m)
     return res
+
+
+def short_name(kernel: str) -> str:
+    base = kernel.replace("void ", "").split("(")[0].split("<")[0].split("::")[-1]
+    return SHORT.get(base, base)
 
 
 def to_bytes(v, unit) -> float:
@@ -74,8 +89,8 @@ def main(src: str, tag: str) -> None:
     if sj.exists():
         summary = json.loads(sj.read_text())
     for rep in sorted(src_p.glob("full_*.ncu-rep")):
-        name = rep.stem.replace("full_", "")
-        m = raw_metrics(rep)
+      for m in raw_metrics(rep):
+        name = short_name(m.get("kernel", "")) or rep.stem.replace("full_", "")
         lines = [f"# ncu --set full --clock-control none, {tag}: {m.get('kernel', '')[:160]}"]
         for k in KEYS:
             if k in m:
