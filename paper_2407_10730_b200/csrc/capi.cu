@@ -118,6 +118,9 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
 int64_t tma_tail_workspace_bytes(const Geom& g, const FusedLayout& L);
 int debug_trace_copy(unsigned long long* host, int max_ctas, int* slots);
 int tma_tail_counters(const Geom& g, const FusedLayout& L);
+int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
+                   const float* bias, float* y, cudaStream_t st);
+int ts_plan_query(const Geom& g, cb_tile_plan* out);
 int ffma_plan_query(const Geom& g, int64_t npix, bool allow_split, cb_tile_plan* out);
 int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
               const void* w_lo, const float* bias, float* out, int add_mode, int zero_kind,
@@ -467,11 +470,11 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
         out->k_blocks = (g.kdim + 15) / 16;
         return CB_OK;
     }
-    out->path = L.tma;
+    out->path = L.ts ? 2 : L.tma;
     out->chunk_channels = L.tma ? L.cb : 0;
     out->chunk_bytes = L.tma ? L.chunk_bytes : 0;
     out->k_blocks = L.tma ? L.num_kb : (g.kdim + 128 / L.eb - 1) / (128 / L.eb);
-    out->weight_cols = L.tma ? L.kw_pad : cb_split_kdim(g.kdim);
+    out->weight_cols = L.tma ? L.kw_pad : cb_split_kdim(g.kdim);  // K7 / K4: plain split rows
     out->workspace_bytes = act_ws_bytes(gk, L);
     return CB_OK;
 }
@@ -483,6 +486,7 @@ int cb_fused_plan_tiles(int variant, const cb_conv_desc* d, cb_tile_plan* plan) 
     if (rc) return rc;
     if (!plan) return fail(CB_ERR_INVALID, "null out pointer");
     if (variant == CB_VARIANT_FFMA) return ffma_plan_query(g, g.npix, true, plan);
+    if (L.ts) return ts_plan_query(g, plan);
     if (L.tma) return tma_plan_query(gk, variant == CB_VARIANT_TC3XBF16, plan);
     return tc_plan_query(g, g.npix, variant == CB_VARIANT_TC3XBF16, true, plan);
 }
@@ -532,6 +536,11 @@ int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, con
     if (!y) return fail(CB_ERR_INVALID, "null output");
     if (d->has_bias && !bias) return fail(CB_ERR_INVALID, "descriptor has bias but bias is null");
     const float* b = d->has_bias ? bias : nullptr;
+    if (variant != CB_VARIANT_FFMA && L.ts) {
+        if (!x) return fail(CB_ERR_INVALID, "null input");
+        if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need packed weights");
+        return launch_conv_ts(g, x, w_hi, w_lo, b, y, (cudaStream_t)stream);
+    }
     if (variant != CB_VARIANT_FFMA && L.tma) {
         if (!ws || (int64_t)ws_bytes < act_ws_bytes(gk, L))
             return fail(CB_ERR_WORKSPACE, "workspace too small: need " +

@@ -129,6 +129,7 @@ struct FusedLayout {
     int64_t act_elems; // N * H * W * c_alloc (per hi / lo buffer)
     int fold;          // 0, or the kernel width S when the horizontal taps are folded into
                        // the channels (small C): the kernel then runs fold_geom(g)
+    int ts;            // 1: the direct TMEM kernel (K7, conv_ts.cu) serves it (tma = 0)
 };
 
 // The same convolution with its S horizontal taps folded into the channel axis: the input

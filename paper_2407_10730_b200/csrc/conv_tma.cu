@@ -583,8 +583,23 @@ static FusedLayout base_layout(const Geom& g, bool bf16) {
 // (few channels: C=3 pads each tap to a 16-byte chunk, 147 -> 392 for a 7x7 stem; folded
 // it is 7 taps of 21 -> 24 channels, 147 -> 256) -- fewer MMAs and fewer, larger TMA boxes.
 // Weights are repacked to match (weight_split_taps, fold) and K0 writes the folded rows.
+bool ts_eligible(const Geom& g);
+
 FusedLayout fused_layout(const Geom& g, bool bf16) {
     FusedLayout L = base_layout(g, bf16);
+    // Few channels (C <= 16): the direct kernel builds A in TMEM from TMA-staged fp32 rows
+    // (no activation pre-pass, no padded taps).  bf16 split only.
+    if (bf16 && g.C <= 16 && !std::getenv("CB_NO_TS") && ts_eligible(g)) {
+        FusedLayout T = L;
+        T.tma = 0;
+        T.fold = 0;
+        T.ts = 1;
+        return T;
+    }
+    if (std::getenv("CB_FORCE_GATHER")) {  // diagnostics: the K4 gather path (no workspace)
+        L.tma = 0;
+        return L;
+    }
     if (g.G == 1 && g.S > 1 && g.C * g.S <= 128 && !std::getenv("CB_NO_FOLD")) {
         FusedLayout F = base_layout(fold_geom(g), bf16);
         if (F.tma && (!L.tma || F.num_kb < L.num_kb)) {

@@ -1,0 +1,452 @@
+// conv_ts.cu -- K7: direct tcgen05 convolution for few-channel layers (short reductions,
+// C*R*S <= ~200, e.g. the 3-channel 7x7 stem of config 3).
+//
+// The TMA path (K0 + K6) pads every tap of a 3-channel conv to a 16-byte chunk and round-
+// trips a re-laid-out copy of the input through HBM; with N = 64 output channels its
+// shared-memory-operand MMAs are bound by the A-operand reads.  Here instead:
+//
+//   * warp 12 (TMA) stages the zero-padded fp32 input rows one 128-pixel tile needs
+//     ([C][rows][W + 2*pw] box of the NCHW tensor, out-of-range rows/cols zero-filled by
+//     the TMA unit) into a double-buffered smem window, and loads the split weights once;
+//   * warps 0-7 (producers, two per TMEM lane quadrant, each half of the K chunks) build
+//     the tile's A operand -- pixel row m, reduction k = (c, r, s) in OIHW order -- from
+//     the window, split every value into bf16 (hi, lo) and write both halves straight into
+//     TMEM with tcgen05.st (no smem A tile, no activation pre-pass, no workspace);
+//   * warp 13 issues, per 16-wide K step, A_lo*B_hi, A_hi*B_lo, A_hi*B_hi as
+//     tcgen05.mma kind::f16 with A read from TMEM and B (weights, K-major SW128) from smem;
+//   * warps 8-11 (epilogue) drain the double-buffered TMEM accumulator into NCHW (+bias).
+//
+// Tiles are 128 consecutive output pixels of one image; the persistent grid walks them.
+// HBM traffic is the algorithmic minimum: x read once (the window re-reads hit L2), y
+// written once, the weights once per CTA.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "cb_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace cb {
+
+constexpr int TS_BM = 128;
+constexpr int TS_PROD_WARPS = 8;
+constexpr int TS_EPI_WARP0 = 8;
+constexpr int TS_TMA_WARP = 12;
+constexpr int TS_MMA_WARP = 13;
+constexpr int TS_THREADS = 14 * 32;
+constexpr int TS_TMEM_COLS = 512;
+
+struct TsParams {
+    Geom g;
+    const float* bias;
+    float* out;
+    int kp;             // reduction padded to 32 (A columns per half: kp / 2)
+    int n_pad;          // output channels padded to 16 (MMA N)
+    int kb_w;           // split weight row length (multiple of 64)
+    int tiles_per_img;  // ceil(PQ / 128)
+    int64_t total_tiles;
+    int box_rows, box_w;    // staging window: input rows x padded row width
+    int x0;                 // window column 0 = input column -x0 (x0 = pw rounded up to 4)
+    uint32_t stage_bytes;   // C * box_rows * box_w * 4 (TMA transaction bytes)
+    uint32_t stage_stride;  // stage_bytes rounded to 1 KB (buffer pitch)
+    uint32_t w_half_bytes;  // n_pad * kb_w * 2
+    int debug;              // diagnostics (CB_TS_DEBUG): 1 no MMA, 2 no tcgen05.st, 4 no input TMA
+    int tma_store;          // 1: epilogue stages 32-channel chunks in smem, TMA stores them
+};
+
+// two fp32 -> packed bf16 pair (round to nearest even), element `lo_elem` in bits 0..15
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo_elem, float hi_elem) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
+    return d;
+}
+
+__global__ void __launch_bounds__(TS_THREADS, 1)
+conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUtensorMap tm_x,
+               const __grid_constant__ CUtensorMap tm_whi, const __grid_constant__ CUtensorMap tm_wlo,
+               const __grid_constant__ CUtensorMap tm_y) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* w_hi = smem;
+    uint8_t* w_lo = smem + p.w_half_bytes;
+    float* stage0 = reinterpret_cast<float*>(smem + 2 * p.w_half_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * p.w_half_bytes + 2 * p.stage_stride);
+    uint64_t* w_full = bars;            // 1
+    uint64_t* s_full = bars + 1;        // 2: staging window landed
+    uint64_t* s_empty = bars + 3;       // 2: producers done with the window
+    uint64_t* a_full = bars + 5;        // 2: A buffer written
+    uint64_t* a_empty = bars + 7;       // 2: MMAs done reading the A buffer
+    uint64_t* acc_full = bars + 9;      // 2: accumulator ready
+    uint64_t* acc_empty = bars + 11;    // 2: epilogue drained the accumulator
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+    // epilogue staging: 2 x [32 channels][128 pixels] fp32 (after the barriers, 1 KB aligned)
+    float* ostage = reinterpret_cast<float*>(smem + 2 * p.w_half_bytes + 2 * p.stage_stride + 1024);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const Geom& g = p.g;
+    const int col_a0 = 2 * p.n_pad;  // TMEM: [acc0 | acc1 | A0 (hi, lo) | A1 (hi, lo)]
+    const int half_cols = p.kp / 2;
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(w_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&s_full[b], 1);
+            ptx::mbar_init(&s_empty[b], 32 * TS_PROD_WARPS);
+            ptx::mbar_init(&a_full[b], 32 * TS_PROD_WARPS);
+            ptx::mbar_init(&a_empty[b], 1);
+            ptx::mbar_init(&acc_full[b], 1);
+            ptx::mbar_init(&acc_empty[b], 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == TS_TMA_WARP && lane == 0) {
+        ptx::tma_prefetch_desc(&tm_x);
+        ptx::tma_prefetch_desc(&tm_whi);
+        ptx::tma_prefetch_desc(&tm_wlo);
+    }
+    if (warp == TS_MMA_WARP) ptx::tmem_alloc(tmem_slot, TS_TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < TS_PROD_WARPS) {
+        // ============================ A producers ======================================
+        // koff[k] = window offset of reduction element k = (c, r, s) relative to the pixel's
+        // window origin (the same for every pixel); k >= kdim points at a finite value
+        // (the matching weight rows are zero).  Per element: one LDS, then the (hi, lo)
+        // split with paired bf16x2 conversions -- no predicates in the loop.
+        int* koff = reinterpret_cast<int*>(ostage + 2 * 32 * TS_BM);
+        for (int k = threadIdx.x; k < p.kp; k += 32 * TS_PROD_WARPS) {
+            int o = 0;
+            if (k < g.kdim) {
+                const int c = k / g.RS, rs = k - (k / g.RS) * g.RS;
+                const int r = rs / g.S, s2 = rs - (rs / g.S) * g.S;
+                o = (c * p.box_rows + r * g.dh) * p.box_w + s2 * g.dw;
+            }
+            koff[k] = o;
+        }
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        const int quad = warp & 3, khalf = warp >> 2;
+        const int m = quad * 32 + lane;  // pixel row of the tile == TMEM lane
+        const uint32_t lane_addr = tmem_base + ((uint32_t)(quad * 32) << 16);
+        const int nchunks = p.kp / 32;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+            const int b = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int n = (int)(t / p.tiles_per_img);
+            const int p0 = (int)(t - (int64_t)n * p.tiles_per_img) * TS_BM;
+            const int oy_a = p0 / g.Q;
+            const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
+            const int oy = pix / g.Q;
+            const int ox = pix - oy * g.Q;
+            const float* xs = stage0 + (size_t)b * (p.stage_stride / 4) +
+                              (size_t)(oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw);
+            ptx::mbar_wait(&s_full[b], ph);
+            ptx::mbar_wait(&a_empty[b], ph ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
+            const uint32_t a_lo = a_hi + half_cols;
+            for (int kc = khalf; kc < nchunks && !(p.debug & 16); kc += 2) {
+                const int4* ko = reinterpret_cast<const int4*>(koff + kc * 32);
+                uint32_t hv[16], lv[16];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int4 o = ko[q];
+                    const float v0 = xs[o.x], v1 = xs[o.y], v2 = xs[o.z], v3 = xs[o.w];
+                    const uint32_t h01 = bf16x2_rn(v0, v1), h23 = bf16x2_rn(v2, v3);
+                    hv[2 * q] = h01;
+                    hv[2 * q + 1] = h23;
+                    lv[2 * q] = bf16x2_rn(v0 - __uint_as_float(h01 << 16),
+                                          v1 - __uint_as_float(h01 & 0xffff0000u));
+                    lv[2 * q + 1] = bf16x2_rn(v2 - __uint_as_float(h23 << 16),
+                                              v3 - __uint_as_float(h23 & 0xffff0000u));
+                }
+                if (!(p.debug & 2)) {
+                    ptx::tmem_st_32x32b_x16(a_hi + kc * 16, hv);
+                    ptx::tmem_st_32x32b_x16(a_lo + kc * 16, lv);
+                }
+            }
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&a_full[b]);
+            ptx::mbar_arrive(&s_empty[b]);
+        }
+    } else if (warp < TS_TMA_WARP) {
+        // ============================ epilogue ==========================================
+        // TMEM -> registers (+bias).  With tma_store: each 32-channel chunk goes to a
+        // double-buffered [32][128] smem tile and one elected thread TMA-stores it (the TMA
+        // unit keeps the HBM writes in flight); otherwise coalesced 128-byte stores.
+        const int quad = warp & 3;
+        const int m = quad * 32 + lane;
+        const bool issuer = threadIdx.x == TS_EPI_WARP0 * 32;
+        int i = 0, chunk = 0;
+        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+            const int b = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int n = (int)(t / p.tiles_per_img);
+            const int p0 = (int)(t - (int64_t)n * p.tiles_per_img) * TS_BM;
+            const int pix = p0 + m;
+            const bool valid = pix < g.PQ;
+            float* dst = p.out + (int64_t)n * g.K * g.PQ + pix;
+            ptx::mbar_wait(&acc_full[b], ph);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < g.K; c0 += 32, ++chunk) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + b * p.n_pad + c0,
+                                        r);
+                ptx::tmem_ld_wait();
+                if (c0 + 32 >= g.K) {  // accumulator fully in registers: release it early
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&acc_empty[b]);
+                }
+                if (p.debug & 8) continue;
+                if (p.tma_store) {
+                    float* buf = ostage + (chunk & 1) * (32 * TS_BM);
+                    if (issuer) ptx::bulk_wait_read<1>();  // the store 2 chunks ago left buf
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int co = c0 + e;
+                        buf[e * TS_BM + m] = __uint_as_float(r[e]) +
+                                             (p.bias && co < g.K ? __ldg(p.bias + co) : 0.f);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (issuer) {
+                        ptx::tma_store_3d(&tm_y, buf, p0, c0, n);
+                        ptx::bulk_commit();
+                    }
+                } else if (valid) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int co = c0 + e;
+                        if (co < g.K)
+                            dst[(int64_t)co * g.PQ] =
+                                __uint_as_float(r[e]) + (p.bias ? __ldg(p.bias + co) : 0.f);
+                    }
+                }
+            }
+        }
+        if (issuer) ptx::bulk_wait_all();
+    } else if (warp == TS_TMA_WARP) {
+        // ============================ TMA: weights once, then input windows =============
+        const uint32_t leader = ptx::elect_one();
+        const int wblocks = p.kb_w / 64;
+        if (leader) {
+            ptx::mbar_arrive_expect_tx(w_full, 2 * p.w_half_bytes);
+            for (int kb = 0; kb < wblocks; ++kb) {
+                ptx::tma_load_2d(w_hi + (size_t)kb * p.n_pad * 128, &tm_whi, w_full, kb * 64, 0);
+                ptx::tma_load_2d(w_lo + (size_t)kb * p.n_pad * 128, &tm_wlo, w_full, kb * 64, 0);
+            }
+        }
+        __syncwarp();
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+            const int b = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int n = (int)(t / p.tiles_per_img);
+            const int p0 = (int)(t - (int64_t)n * p.tiles_per_img) * TS_BM;
+            const int iy0 = (p0 / g.Q) * g.sh - g.ph;
+            ptx::mbar_wait(&s_empty[b], ph ^ 1);
+            if (leader && (p.debug & 4)) {
+                ptx::mbar_arrive(&s_full[b]);
+            } else if (leader) {
+                ptx::mbar_arrive_expect_tx(&s_full[b], p.stage_bytes);
+                ptx::tma_load_4d(reinterpret_cast<uint8_t*>(stage0) + (size_t)b * p.stage_stride, &tm_x,
+                                 &s_full[b], -p.x0, iy0, 0, n);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ============================ MMA issuer ========================================
+        const uint32_t leader = ptx::elect_one();
+        const uint32_t idesc = ptx::idesc_f32acc<true>(TS_BM, p.n_pad);
+        const uint64_t dbh0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_hi));
+        const uint64_t dbl0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_lo));
+        const uint32_t blk16 = (uint32_t)(p.n_pad * 128) >> 4;  // one 64-wide K block of B
+        const int ksteps = p.kp / 16;
+        ptx::mbar_wait(w_full, 0);
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+            const int b = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            ptx::mbar_wait(&a_full[b], ph);
+            ptx::mbar_wait(&acc_empty[b], ph ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_base + b * p.n_pad;
+            const uint32_t a_hi = tmem_base + col_a0 + b * p.kp;
+            const uint32_t a_lo = a_hi + half_cols;
+            if (leader) {
+                for (int j = 0; j < ksteps && !(p.debug & 1); ++j) {
+                    const uint64_t boff = (uint64_t)((j >> 2) * blk16 + (j & 3) * 2);
+                    ptx::umma_ts_bf16(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
+                    ptx::umma_ts_bf16(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
+                    ptx::umma_ts_bf16(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
+                }
+                ptx::umma_commit(&a_empty[b]);
+                ptx::umma_commit(&acc_full[b]);
+            }
+            __syncwarp();
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == TS_MMA_WARP) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, TS_TMEM_COLS);
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// Host side
+// ----------------------------------------------------------------------------------------
+struct TsPlan {
+    bool ok;
+    int kp, n_pad, kb_w, box_rows, box_w, x0;
+    uint32_t stage_bytes, stage_stride, w_half_bytes;
+    bool tma_store;
+    size_t smem;
+};
+
+static TsPlan plan_ts(const Geom& g) {
+    TsPlan pl{};
+    if (g.G != 1 || g.npix == 0) return pl;
+    pl.kp = round_up(g.kdim, 32);
+    pl.n_pad = round_up(g.K, 16);
+    pl.kb_w = round_up(g.kdim, 64);  // == cb_split_kdim(kdim)
+    if (pl.n_pad > 256 || 2 * pl.n_pad + 2 * pl.kp > TS_TMEM_COLS) return pl;
+    pl.x0 = round_up(g.pw, 4);  // 16-byte aligned window start
+    pl.box_w = round_up(g.W + g.pw + pl.x0, 4);
+    const int out_rows = std::min(g.P, (TS_BM - 1) / std::max(1, g.Q) + 2);
+    pl.box_rows = (out_rows - 1) * g.sh + (g.R - 1) * g.dh + 1;
+    if (pl.box_w > 256 || pl.box_rows > 256 || g.C > 256 || (g.W % 4) != 0) return pl;
+    pl.stage_bytes = (uint32_t)g.C * pl.box_rows * pl.box_w * 4;
+    pl.stage_stride = (pl.stage_bytes + 1023) / 1024 * 1024;
+    pl.w_half_bytes = (uint32_t)pl.n_pad * pl.kb_w * 2;
+    // >= 120 KB keeps one CTA per SM (each allocates all 512 TMEM columns)
+    pl.tma_store = (g.PQ % 4) == 0;  // 16-byte global strides for the output map
+    pl.smem = std::max<size_t>(120 * 1024, 1024 + 2 * (size_t)pl.w_half_bytes +
+                                               2 * (size_t)pl.stage_stride + 1024 +
+                                               2 * 32 * TS_BM * 4 + 4 * (size_t)pl.kp);
+    pl.ok = pl.stage_bytes <= 64 * 1024 && pl.smem <= 227 * 1024;
+    return pl;
+}
+
+// Used by fused_layout: the direct kernel serves this descriptor (bf16 split only).
+bool ts_eligible(const Geom& g) { return plan_ts(g).ok; }
+
+int ts_plan_query(const Geom& g, cb_tile_plan* out) {
+    const TsPlan pl = plan_ts(g);
+    if (!pl.ok) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
+    const int64_t tiles = (int64_t)g.N * ((g.PQ + TS_BM - 1) / TS_BM);
+    out->variant = CB_VARIANT_TC3XBF16;
+    out->block_m = TS_BM;
+    out->block_n = pl.n_pad;
+    out->block_k = 16;
+    out->stages = 2;
+    out->splits = 1;
+    out->m_tiles = tiles;
+    out->n_tiles = 1;
+    out->k_blocks = pl.kp / 16;
+    out->ctas = (int)std::min<int64_t>(tiles, sm_count());
+    return CB_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 ts_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
+                   const float* bias, float* y, cudaStream_t st) {
+    const TsPlan pl = plan_ts(g);
+    if (!pl.ok) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
+    auto enc = ts_encode_fn();
+    if (!enc) return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w_hi) |
+         reinterpret_cast<uintptr_t>(w_lo)) & 15)
+        return fail(CB_ERR_MISALIGNED, "input and packed weights must be 16-byte aligned");
+    CUtensorMap mx, mwh, mwl, my{};
+    {
+        cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.C, (cuuint64_t)g.N};
+        cuuint64_t strides[3] = {(cuuint64_t)g.W * 4, (cuuint64_t)g.HW * 4,
+                                 (cuuint64_t)g.C * g.HW * 4};
+        cuuint32_t box[4] = {(cuuint32_t)pl.box_w, (cuuint32_t)pl.box_rows, (cuuint32_t)g.C, 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (input) failed: " + std::to_string((int)r));
+    }
+    for (int h = 0; h < 2; ++h) {
+        cuuint64_t dims[2] = {(cuuint64_t)pl.kb_w, (cuuint64_t)g.K};
+        cuuint64_t strides[1] = {(cuuint64_t)pl.kb_w * 2};
+        cuuint32_t box[2] = {64, (cuuint32_t)pl.n_pad};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(h ? &mwl : &mwh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                         const_cast<void*>(h ? w_lo : w_hi), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string((int)r));
+    }
+    if (pl.tma_store) {
+        if (reinterpret_cast<uintptr_t>(y) & 15)
+            return fail(CB_ERR_MISALIGNED, "output must be 16-byte aligned");
+        cuuint64_t dims[3] = {(cuuint64_t)g.PQ, (cuuint64_t)g.K, (cuuint64_t)g.N};
+        cuuint64_t strides[2] = {(cuuint64_t)g.PQ * 4, (cuuint64_t)g.K * g.PQ * 4};
+        cuuint32_t box[3] = {(cuuint32_t)TS_BM, 32, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = enc(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, y, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string((int)r));
+    }
+    TsParams prm{};
+    prm.tma_store = pl.tma_store ? 1 : 0;
+    if (std::getenv("CB_TS_NO_TMA_STORE")) prm.tma_store = 0;
+    prm.g = g;
+    prm.bias = bias;
+    prm.out = y;
+    prm.kp = pl.kp;
+    prm.n_pad = pl.n_pad;
+    prm.kb_w = pl.kb_w;
+    prm.tiles_per_img = (g.PQ + TS_BM - 1) / TS_BM;
+    prm.total_tiles = (int64_t)g.N * prm.tiles_per_img;
+    prm.box_rows = pl.box_rows;
+    prm.box_w = pl.box_w;
+    prm.x0 = pl.x0;
+    prm.stage_bytes = pl.stage_bytes;
+    prm.stage_stride = pl.stage_stride;
+    prm.w_half_bytes = pl.w_half_bytes;
+    if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(conv_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024);
+    });
+    if (attr_err != cudaSuccess)
+        return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    const int grid = (int)std::min<int64_t>(prm.total_tiles, sm_count());
+    conv_ts_kernel<<<grid, TS_THREADS, pl.smem, st>>>(prm, mx, mwh, mwl, my);
+    return check_launch("conv_ts_kernel");
+}
+
+}  // namespace cb
