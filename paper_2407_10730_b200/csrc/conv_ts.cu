@@ -29,11 +29,11 @@
 namespace cb {
 
 constexpr int TS_BM = 128;
-constexpr int TS_PROD_WARPS = 8;
-constexpr int TS_EPI_WARP0 = 8;
-constexpr int TS_TMA_WARP = 12;
-constexpr int TS_MMA_WARP = 13;
-constexpr int TS_THREADS = 14 * 32;
+constexpr int TS_PROD_WARPS = 12;  // three per TMEM lane quadrant
+constexpr int TS_EPI_WARP0 = 12;
+constexpr int TS_TMA_WARP = 16;
+constexpr int TS_MMA_WARP = 17;
+constexpr int TS_THREADS = 18 * 32;
 constexpr int TS_TMEM_COLS = 512;
 
 struct TsParams {
@@ -53,6 +53,19 @@ struct TsParams {
     int debug;              // diagnostics (CB_TS_DEBUG): 1 no MMA, 2 no tcgen05.st, 4 no input TMA
     int tma_store;          // 1: epilogue stages 32-channel chunks in smem, TMA stores them
 };
+
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
 
 // two fp32 -> packed bf16 pair (round to nearest even), element `lo_elem` in bits 0..15
 __device__ __forceinline__ uint32_t bf16x2_rn(float lo_elem, float hi_elem) {
@@ -126,10 +139,11 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 const int r = rs / g.S, s2 = rs - (rs / g.S) * g.S;
                 o = (c * p.box_rows + r * g.dh) * p.box_w + s2 * g.dw;
             }
-            koff[k] = o;
+            koff[k] = 4 * o;  // byte offset
         }
-        asm volatile("bar.sync 2, 256;" ::: "memory");
-        const int quad = warp & 3, khalf = warp >> 2;
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * TS_PROD_WARPS) : "memory");
+        const int quad = warp & 3, kpart = warp >> 2;
+        constexpr int KPARTS = TS_PROD_WARPS / 4;
         const int m = quad * 32 + lane;  // pixel row of the tile == TMEM lane
         const uint32_t lane_addr = tmem_base + ((uint32_t)(quad * 32) << 16);
         const int nchunks = p.kp / 32;
@@ -143,20 +157,21 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
             const int oy = pix / g.Q;
             const int ox = pix - oy * g.Q;
-            const float* xs = stage0 + (size_t)b * (p.stage_stride / 4) +
-                              (size_t)(oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw);
+            const uint32_t xs = ptx::smem_u32(stage0) + b * p.stage_stride +
+                                4u * (uint32_t)((oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw));
             ptx::mbar_wait(&s_full[b], ph);
             ptx::mbar_wait(&a_empty[b], ph ^ 1);
             ptx::tc_fence_after();
             const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
             const uint32_t a_lo = a_hi + half_cols;
-            for (int kc = khalf; kc < nchunks && !(p.debug & 16); kc += 2) {
-                const int4* ko = reinterpret_cast<const int4*>(koff + kc * 32);
+            for (int kc = kpart; kc < nchunks && !(p.debug & 16); kc += KPARTS) {
+                const uint32_t ko = ptx::smem_u32(koff + kc * 32);
                 uint32_t hv[16], lv[16];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const int4 o = ko[q];
-                    const float v0 = xs[o.x], v1 = xs[o.y], v2 = xs[o.z], v3 = xs[o.w];
+                    const int4 o = lds_v4(ko + 16 * q);
+                    const float v0 = lds_f32(xs + o.x), v1 = lds_f32(xs + o.y);
+                    const float v2 = lds_f32(xs + o.z), v3 = lds_f32(xs + o.w);
                     const uint32_t h01 = bf16x2_rn(v0, v1), h23 = bf16x2_rn(v2, v3);
                     hv[2 * q] = h01;
                     hv[2 * q + 1] = h23;
@@ -209,11 +224,14 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                     float* buf = ostage + (chunk & 1) * (32 * TS_BM);
                     if (issuer) ptx::bulk_wait_read<1>();  // the store 2 chunks ago left buf
                     asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (p.bias) {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int co = c0 + e;
-                        buf[e * TS_BM + m] = __uint_as_float(r[e]) +
-                                             (p.bias && co < g.K ? __ldg(p.bias + co) : 0.f);
+                        for (int e = 0; e < 32; ++e)
+                            buf[e * TS_BM + m] = __uint_as_float(r[e]) +
+                                                 (c0 + e < g.K ? __ldg(p.bias + c0 + e) : 0.f);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) buf[e * TS_BM + m] = __uint_as_float(r[e]);
                     }
                     ptx::fence_proxy_async_smem();
                     asm volatile("bar.sync 1, 128;" ::: "memory");

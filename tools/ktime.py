@@ -24,6 +24,9 @@ from paper_2407_10730_b200.configs import CONFIGS, conv_flops
 
 def run(name: str, variant: str, reps: int = 20) -> None:
     d = CONFIGS[name]
+    if os.environ.get("CB_KT_BATCH"):  # diagnostics: same layer, another batch size
+        from dataclasses import replace
+        d = replace(d, batch=int(os.environ["CB_KT_BATCH"]))
     rng = np.random.default_rng(0)
     x = torch.from_numpy(rng.random((d.batch, d.in_channels, d.in_h, d.in_w), dtype=np.float32) * 2 - 1).cuda()
     w = torch.from_numpy(rng.random((d.out_channels, d.in_channels, d.k_h, d.k_w), dtype=np.float32) * 2 - 1).cuda()
@@ -35,19 +38,19 @@ def run(name: str, variant: str, reps: int = 20) -> None:
     ws = algos.fused_workspace(d, variant)
     nbytes = ws.numel() if ws is not None else 0
     wsp = ws.data_ptr() if ws is not None else None
-    st = torch.cuda.current_stream().cuda_stream
+    cur = lambda: torch.cuda.current_stream().cuda_stream  # graph capture uses its own stream
     ptr = lambda t: None if t is None else t.data_ptr()
 
     def k0():
-        _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), x.data_ptr(), wsp, nbytes, st))
+        _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), x.data_ptr(), wsp, nbytes, cur()))
 
     def k6():
         _capi.check(lib.cb_conv_fused_packed(vid, ctypes.byref(cd), x.data_ptr(), wsp, nbytes,
-                                             ptr(hi), ptr(lo), ptr(wf), None, y.data_ptr(), st))
+                                             ptr(hi), ptr(lo), ptr(wf), None, y.data_ptr(), cur()))
 
     def k3():
         _capi.check(lib.cb_fused_pack_weights(vid, ctypes.byref(cd), w.data_ptr(), ptr(hi),
-                                              ptr(lo), st))
+                                              ptr(lo), cur()))
 
     k0()
     res = {}
@@ -58,13 +61,19 @@ def run(name: str, variant: str, reps: int = 20) -> None:
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
+        # device time: the reps launches replay from one CUDA graph (no host gaps)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(reps):
+                fn()
+        graph.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sampler = Clocks(0) if label == "K6" else None
         if sampler:
             sampler.__enter__()
         e0.record()
-        for _ in range(reps):
-            fn()
+        graph.replay()
         e1.record()
         torch.cuda.synchronize()
         if sampler:
