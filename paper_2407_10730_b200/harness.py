@@ -56,6 +56,9 @@ class RunConfig:
     rtol: float = DEFAULT_RTOL
     atol: float = DEFAULT_ATOL
     variant: str = algos.DEFAULT_VARIANT
+    # device ledgers only: capture the timed op once into a CUDA graph (external phase events)
+    # and replay it for warmups and runs -- phases then time the kernels, not host launches
+    graph: bool = False
 
     def __post_init__(self) -> None:
         if self.mode not in MODES:
@@ -170,15 +173,31 @@ def run_single(desc: ConvDescriptor, cfg: RunConfig, main_fn: ConvFn | None = No
         else:
             host = make_inputs(desc, cfg)
             inputs = to_device(host)
-        ledger = ledger_factory()
-        for _ in range(cfg.warmups):
-            ledger.reset()
-            timed(inputs, ledger)
         reports = []
-        for _ in range(cfg.runs):
-            ledger.reset()
-            timed(inputs, ledger)
-            reports.append(ledger.snapshot())
+        if cfg.graph and ledger_factory is EventLedger:
+            import torch
+            timed(inputs, EventLedger())  # eager first call: plans, attributes, tensor maps
+            ledger = EventLedger(external=True)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=side):
+                timed(inputs, ledger)
+            for _ in range(cfg.warmups):
+                graph.replay()
+            for _ in range(cfg.runs):
+                graph.replay()
+                reports.append(ledger.snapshot())  # the latest replay's events
+            del graph
+        else:
+            ledger = ledger_factory()
+            for _ in range(cfg.warmups):
+                ledger.reset()
+                timed(inputs, ledger)
+            for _ in range(cfg.runs):
+                ledger.reset()
+                timed(inputs, ledger)
+                reports.append(ledger.snapshot())
         out = outcome("ok", stats=aggregate(reports))
         if cfg.mode == "correctness":
             got = _as_numpy(main_fn(inputs, PhaseLedger()))

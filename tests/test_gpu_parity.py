@@ -224,3 +224,15 @@ def test_host_pipeline_matches_dropin(cuda, name):
     flipped = conv_fused(_inputs(d)[0].__class__(desc=d, input=x[:, ::-1].copy(), weights=w))
     assert np.array_equal(ys[1].numpy(), flipped)
     _check_conv(d, ys[0].numpy(), orc.conv_direct_naive(d, x, w, b))
+
+
+@pytest.mark.parametrize("mode", ["fused", "baseline", "main"])
+def test_run_single_graph_mode(cuda, mode):
+    """Graph-replayed timing reports the same phases and call counts as eager timing."""
+    from paper_2407_10730_b200.harness import RunConfig, run_single
+    d = cfg("cfg1")
+    eager = run_single(d, RunConfig(mode=mode, warmups=1, runs=2))
+    graph = run_single(d, RunConfig(mode=mode, warmups=1, runs=3, graph=True))
+    assert eager.status == graph.status == "ok", (eager.detail, graph.detail)
+    assert dict(graph.stats.calls) == dict(eager.stats.calls)
+    assert graph.stats.operation_ns_mean > 0

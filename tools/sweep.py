@@ -80,6 +80,8 @@ def main(argv=None) -> int:
     ap.add_argument("--variant", default=None, help="stepwise variant (default tc3xtf32)")
     ap.add_argument("--fused-variant", default=algos.FUSED_DEFAULT_VARIANT)
     ap.add_argument("--device-inputs", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time each op as a replayed CUDA graph (kernels without host launch gaps)")
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip larger ops (0: none)")
     ap.add_argument("--out", default="sweep_out")
     args = ap.parse_args(argv)
@@ -109,7 +111,7 @@ def main(argv=None) -> int:
     for m in modes:
         variant = args.fused_variant if m == "fused" else (args.variant or algos.DEFAULT_VARIANT)
         cfg = harness.RunConfig(mode=m, warmups=args.warmups, runs=args.runs,
-                                seed=args.data_seed, variant=variant)
+                                seed=args.data_seed, variant=variant, graph=args.graph)
         for n, i in enumerate(mine):
             o = harness.run_single(descs[i], cfg, inputs_fn=inputs_fn)
             rf = roofline.conv_roofline(descs[i], variant, peaks)
@@ -140,7 +142,10 @@ def main(argv=None) -> int:
                    "data_seed": args.data_seed, "sample": args.sample, "world": world,
                    "inputs": "device (torch.rand, not make_inputs bits)" if args.device_inputs
                    else "make_inputs (bit-identical to the reference)",
-                   "warmups": args.warmups, "runs": args.runs, "peaks": peaks, "modes": {}}
+                   "warmups": args.warmups, "runs": args.runs, "peaks": peaks,
+                   "timing": "CUDA-graph replay per op (device phases, no host launch gaps)"
+                   if args.graph else "eager calls (device phases include launch latency)",
+                   "modes": {}}
         for m in modes:
             rows = sorted((r for g in gathered for r in g["rows"][m]), key=lambda r: r["index"])
             report.write_results_csv([r["record"] for r in rows], out / f"results_{m}.csv")
