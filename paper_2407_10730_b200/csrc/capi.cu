@@ -111,7 +111,9 @@ FusedLayout fused_layout(const Geom& g, bool bf16);
 int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
                      int* counters, int n_counters, cudaStream_t st, int fold);
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
-                             void* hi, void* lo, cudaStream_t st, int fold);
+                             void* hi, void* lo, cudaStream_t st, int fold, int stack_rs,
+                             int k_orig);
+int launch_tap_sum(const Geom& g, const float* yp, const float* bias, float* y, cudaStream_t st);
 int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* act_hi,
                     const void* act_lo, const void* w_hi, const void* w_lo, const float* bias,
                     float* y, void* tail_ws, cudaStream_t st);
@@ -440,7 +442,7 @@ static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout*
         return fail(CB_ERR_UNSUPPORTED, "unknown variant " + std::to_string(variant));
     *L = FusedLayout{};
     if (variant != CB_VARIANT_FFMA) *L = fused_layout(*g, variant == CB_VARIANT_TC3XBF16);
-    if (gk) *gk = L->fold ? fold_geom(*g) : *g;
+    if (gk) *gk = L->stack ? stack_geom(*g) : L->fold ? fold_geom(*g) : *g;
     return CB_OK;
 }
 
@@ -454,7 +456,15 @@ static void act_halves(const FusedLayout& L, void* ws, void** hi, void** lo, voi
 
 static int64_t act_ws_bytes(const Geom& g, const FusedLayout& L) {
     if (!L.tma) return 0;
-    return 2 * (((int64_t)L.act_elems * L.eb + 255) / 256 * 256) + tma_tail_workspace_bytes(g, L);
+    const int64_t tail = (tma_tail_workspace_bytes(g, L) + 255) / 256 * 256;
+    // stacked taps: + the 1x1 conv's output Y' (fp32 NCHW over the input grid)
+    const int64_t stacked = L.stack ? (int64_t)g.N * g.K * g.PQ * 4 : 0;
+    return 2 * (((int64_t)L.act_elems * L.eb + 255) / 256 * 256) + tail + stacked;
+}
+static float* stack_buffer(const Geom& gk, const FusedLayout& L, void* ws) {
+    const int64_t tail = (tma_tail_workspace_bytes(gk, L) + 255) / 256 * 256;
+    return reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
+                                    2 * (((int64_t)L.act_elems * L.eb + 255) / 256 * 256) + tail);
 }
 
 int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* out) {
@@ -464,7 +474,7 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
     if (rc) return rc;
     if (!out) return fail(CB_ERR_INVALID, "null out pointer");
     *out = cb_fused_layout{};
-    out->weight_rows = g.K;
+    out->weight_rows = gk.K;  // stacked taps: R*S*K rows
     if (variant == CB_VARIANT_FFMA) {
         out->path = 0;
         out->k_blocks = (g.kdim + 15) / 16;
@@ -503,7 +513,7 @@ int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, vo
     const bool bf16 = variant == CB_VARIANT_TC3XBF16;
     if (L.tma)
         return launch_weight_split_taps(bf16, gk, L.cb, L.chk, L.kw_pad, w, w_hi, w_lo,
-                                        (cudaStream_t)stream, L.fold);
+                                        (cudaStream_t)stream, L.fold, L.stack, g.K);
     return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
                                (cudaStream_t)stream);
 }
@@ -548,6 +558,13 @@ int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, con
         if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need packed weights");
         void *hi, *lo, *tail;
         act_halves(L, const_cast<void*>(ws), &hi, &lo, &tail);
+        if (L.stack) {  // 1x1 conv into Y', then K9 sums the shifted taps (+bias) into y
+            float* yp = stack_buffer(gk, L, const_cast<void*>(ws));
+            rc = launch_conv_tma(variant == CB_VARIANT_TC3XBF16, gk, L, hi, lo, w_hi, w_lo, nullptr,
+                                 yp, tail, (cudaStream_t)stream);
+            if (rc) return rc;
+            return launch_tap_sum(g, yp, b, y, (cudaStream_t)stream);
+        }
         return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, gk, L, hi, lo, w_hi, w_lo, b, y, tail,
                                (cudaStream_t)stream);
     }

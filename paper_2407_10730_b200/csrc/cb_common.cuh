@@ -130,7 +130,31 @@ struct FusedLayout {
     int fold;          // 0, or the kernel width S when the horizontal taps are folded into
                        // the channels (small C): the kernel then runs fold_geom(g)
     int ts;            // 1: the direct TMEM kernel (K7, conv_ts.cu) serves it (tma = 0)
+    int stack;         // 0, or R*S when the taps are stacked into the output channels: the
+                       // kernel runs stack_geom(g) into a workspace, K9 sums the shifted taps
 };
+
+// Tap stacking (few output channels, many input channels): the R*S taps become output
+// channels of a 1x1 conv over the input grid, Y'[n][rs*K + f][h][w] = sum_c x[n][c][h][w] *
+// w[f][c][r][s]; y[n][f][oy][ox] = sum_rs Y'[n][rs*K + f][oy*sh - ph + r*dh][ox*sw - pw +
+// s*dw].  x is read once instead of once per tap.  groups == 1 only.
+inline Geom stack_geom(const Geom& g) {
+    Geom t = g;
+    t.K = g.R * g.S * g.K;
+    t.kpg = t.K;
+    t.R = t.S = 1;
+    t.sh = t.sw = 1;
+    t.ph = t.pw = 0;
+    t.dh = t.dw = 1;
+    t.P = g.H;
+    t.Q = g.W;
+    t.PQ = g.HW;
+    t.RS = 1;
+    t.kdim = g.cpg;
+    t.kdim_pad = (t.kdim + 63) / 64 * 64;
+    t.npix = (int64_t)g.N * g.HW;
+    return t;
+}
 
 // The same convolution with its S horizontal taps folded into the channel axis: the input
 // becomes [N][H][Q][S*C] (x at column ox*sw + s*dw - pw for channel s*C + c, zero outside)

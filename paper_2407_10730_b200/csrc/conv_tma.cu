@@ -587,6 +587,15 @@ bool ts_eligible(const Geom& g);
 
 FusedLayout fused_layout(const Geom& g, bool bf16) {
     FusedLayout L = base_layout(g, bf16);
+    // Few output channels, many input channels: stack the taps (see stack_geom).  The TMA
+    // im2col walk would re-read every input pixel once per tap for a handful of MMA columns.
+    if (g.G == 1 && g.RS > 1 && g.RS * g.K <= 256 && g.C >= 128 && !std::getenv("CB_NO_STACK")) {
+        FusedLayout T = base_layout(stack_geom(g), bf16);
+        if (T.tma) {
+            T.stack = g.RS;
+            return T;
+        }
+    }
     // Few channels (C <= 16): the direct kernel builds A in TMEM from TMA-staged fp32 rows
     // (no activation pre-pass, no padded taps).  bf16 split only.
     if (bf16 && g.C <= 16 && !std::getenv("CB_NO_TS") && ts_eligible(g)) {

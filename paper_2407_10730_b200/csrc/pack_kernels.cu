@@ -534,7 +534,7 @@ template <bool BF16>
 __global__ void __launch_bounds__(256)
 weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_pad,
                          const float* __restrict__ w, void* __restrict__ hi_out,
-                         void* __restrict__ lo_out, int fold) {
+                         void* __restrict__ lo_out, int fold, int stack_rs, int k_orig) {
     constexpr int VEC = BF16 ? 8 : 4;
     extern __shared__ float ws_tile[];  // [WS_CH][R*S]
     const int f = blockIdx.y;
@@ -544,8 +544,15 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
     const int nch = min(WS_CH, cpg - c0);  // real channels in this chunk (may be <= 0)
     // folded (fold = original S, S == 1 here, one chunk): stage all of w[f] in OIHW order
     // and read channel c' = s*C + c of tap r from w[f, c, r, s]
-    const float* src = w + ((int64_t)f * cpg + c0) * RS;
-    for (int i = threadIdx.x; i < max(nch, 0) * RS; i += 256) ws_tile[i] = __ldg(src + i);
+    // stacked taps (stack_rs > 1, here R = S = 1): row f = rs*K + fo reads w[fo, c, r, s]
+    if (stack_rs > 1) {
+        const int fo = f % k_orig, rs = f / k_orig;
+        const float* srcs = w + ((int64_t)fo * cpg + c0) * stack_rs + rs;
+        for (int i = threadIdx.x; i < max(nch, 0); i += 256) ws_tile[i] = __ldg(srcs + (int64_t)i * stack_rs);
+    } else {
+        const float* src = w + ((int64_t)f * cpg + c0) * RS;
+        for (int i = threadIdx.x; i < max(nch, 0) * RS; i += 256) ws_tile[i] = __ldg(src + i);
+    }
     __syncthreads();
     const int c_orig = fold ? cpg / fold : 0;
     const int cw = min(WS_CH, per_tap - c0);  // output channels of this chunk per tap
@@ -605,7 +612,8 @@ int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void
 }
 
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
-                             void* hi, void* lo, cudaStream_t st, int fold) {
+                             void* hi, void* lo, cudaStream_t st, int fold, int stack_rs,
+                             int k_orig) {
     if (fold && (g.G != 1 || g.S != 1 || chk * CB > WS_CH))
         return fail(CB_ERR_INVALID, "folded weight pack needs one chunk of an R x 1 kernel");
     if ((int64_t)g.K * kw_pad == 0) return CB_OK;
@@ -622,7 +630,8 @@ int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_p
                                              (int)smem);
         if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
     }
-    kern<<<grid, 256, smem, st>>>(g.K, g.cpg, g.R, g.S, CB, chk, kw_pad, w, hi, lo, fold);
+    kern<<<grid, 256, smem, st>>>(g.K, g.cpg, g.R, g.S, CB, chk, kw_pad, w, hi, lo, fold, stack_rs,
+                                  k_orig);
     return check_launch("weight_split_taps");
 }
 
@@ -635,6 +644,46 @@ int pre_init_output(const Geom& g, const PixMap& pm, int zero_kind, const float*
         return CB_OK;
     }
     return fail(CB_ERR_INVALID, "output cannot be pre-initialised for split-K");
+}
+
+}  // namespace cb
+
+namespace cb {
+
+// K9 (stacked taps): y[n][f][oy][ox] = bias[f] + sum_{r,s} Y'[n][(r*S+s)*K + f][iy][ix],
+// iy = oy*sh - ph + r*dh, ix = ox*sw - pw + s*dw (taps outside the image contribute 0),
+// summed in the fixed (r, s) order.  One thread per output, consecutive threads along ox.
+__global__ void __launch_bounds__(256)
+tap_sum_kernel(Geom g, const float* __restrict__ yp, const float* __restrict__ bias,
+               float* __restrict__ y) {
+    const int64_t total = (int64_t)g.N * g.K * g.PQ;
+    for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (int64_t)gridDim.x * 256) {
+        const int64_t nf = i / g.PQ;
+        const int pq = (int)(i - nf * g.PQ);
+        const int64_t n = nf / g.K;
+        const int f = (int)(nf - n * g.K);
+        const int oy = pq / g.Q, ox = pq - (pq / g.Q) * g.Q;
+        float acc = bias ? __ldg(bias + f) : 0.f;
+        const float* base = yp + (n * g.RS * g.K + f) * (int64_t)g.HW;
+        for (int r = 0; r < g.R; ++r) {
+            const int iy = oy * g.sh - g.ph + r * g.dh;
+            if ((unsigned)iy >= (unsigned)g.H) continue;
+            for (int s = 0; s < g.S; ++s) {
+                const int ix = ox * g.sw - g.pw + s * g.dw;
+                if ((unsigned)ix < (unsigned)g.W)
+                    acc += __ldg(base + (int64_t)(r * g.S + s) * g.K * g.HW + iy * g.W + ix);
+            }
+        }
+        y[i] = acc;
+    }
+}
+
+int launch_tap_sum(const Geom& g, const float* yp, const float* bias, float* y, cudaStream_t st) {
+    const int64_t total = (int64_t)g.N * g.K * g.PQ;
+    if (total == 0) return CB_OK;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
+    tap_sum_kernel<<<blocks, 256, 0, st>>>(g, yp, bias, y);
+    return check_launch("tap_sum");
 }
 
 }  // namespace cb

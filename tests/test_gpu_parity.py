@@ -236,3 +236,26 @@ def test_run_single_graph_mode(cuda, mode):
     assert eager.status == graph.status == "ok", (eager.detail, graph.detail)
     assert dict(graph.stats.calls) == dict(eager.stats.calls)
     assert graph.stats.operation_ns_mean > 0
+
+
+STACKED = [  # few output channels, many input channels: the stacked-tap path (fused path 3)
+    dict(batch=2, in_channels=128, in_h=17, in_w=23, out_channels=8, k_h=3, k_w=3, stride_h=1,
+         stride_w=1, pad_h=1, pad_w=1, has_bias=True),
+    dict(batch=1, in_channels=256, in_h=20, in_w=20, out_channels=16, k_h=3, k_w=3, stride_h=2,
+         stride_w=2, pad_h=1, pad_w=1),
+    dict(batch=1, in_channels=192, in_h=15, in_w=16, out_channels=4, k_h=5, k_w=5, stride_h=1,
+         stride_w=1, pad_h=2, pad_w=2, dil_h=2, dil_w=2, has_bias=True),
+    dict(batch=3, in_channels=160, in_h=9, in_w=11, out_channels=10, k_h=1, k_w=7, stride_h=1,
+         stride_w=2, pad_h=0, pad_w=3),
+]
+
+
+@pytest.mark.parametrize("variant", ["tc3xbf16", "tc3xtf32"])
+@pytest.mark.parametrize("spec", range(len(STACKED)))
+def test_stacked_taps_match_oracle(cuda, variant, spec):
+    from paper_2407_10730_b200.algos import conv_fused, fused_layout
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    d = ConvDescriptor(**STACKED[spec])
+    assert fused_layout(d, variant)["path"] == 1  # TMA kernel on the stacked 1x1 geometry
+    inp, (x, w, b) = _inputs(d)
+    _check_conv(d, conv_fused(inp, variant=variant), orc.conv_direct_naive(d, x, w, b))
