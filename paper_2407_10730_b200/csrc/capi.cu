@@ -113,7 +113,8 @@ int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void
 int launch_weight_split_taps(bool bf16, const Geom& g, int CB, int chk, int kw_pad, const float* w,
                              void* hi, void* lo, cudaStream_t st, int fold, int stack_rs,
                              int k_orig);
-int launch_tap_sum(const Geom& g, const float* yp, const float* bias, float* y, cudaStream_t st);
+int launch_tap_sum(const Geom& g, int mode, const float* yp, const float* bias, float* y,
+                   cudaStream_t st);
 int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* act_hi,
                     const void* act_lo, const void* w_hi, const void* w_lo, const float* bias,
                     float* y, void* tail_ws, cudaStream_t st);
@@ -442,7 +443,7 @@ static int fused_setup(int variant, const cb_conv_desc* d, Geom* g, FusedLayout*
         return fail(CB_ERR_UNSUPPORTED, "unknown variant " + std::to_string(variant));
     *L = FusedLayout{};
     if (variant != CB_VARIANT_FFMA) *L = fused_layout(*g, variant == CB_VARIANT_TC3XBF16);
-    if (gk) *gk = L->stack ? stack_geom(*g) : L->fold ? fold_geom(*g) : *g;
+    if (gk) *gk = L->stack ? stack_geom(*g, L->stack) : L->fold ? fold_geom(*g) : *g;
     return CB_OK;
 }
 
@@ -513,7 +514,8 @@ int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, vo
     const bool bf16 = variant == CB_VARIANT_TC3XBF16;
     if (L.tma)
         return launch_weight_split_taps(bf16, gk, L.cb, L.chk, L.kw_pad, w, w_hi, w_lo,
-                                        (cudaStream_t)stream, L.fold, L.stack, g.K);
+                                        (cudaStream_t)stream, L.fold,
+                                        L.stack == 1 ? g.RS : L.stack == 2 ? g.S : 0, g.K);
     return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
                                (cudaStream_t)stream);
 }
@@ -563,7 +565,7 @@ int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, con
             rc = launch_conv_tma(variant == CB_VARIANT_TC3XBF16, gk, L, hi, lo, w_hi, w_lo, nullptr,
                                  yp, tail, (cudaStream_t)stream);
             if (rc) return rc;
-            return launch_tap_sum(g, yp, b, y, (cudaStream_t)stream);
+            return launch_tap_sum(g, L.stack, yp, b, y, (cudaStream_t)stream);
         }
         return launch_conv_tma(variant == CB_VARIANT_TC3XBF16, gk, L, hi, lo, w_hi, w_lo, b, y, tail,
                                (cudaStream_t)stream);

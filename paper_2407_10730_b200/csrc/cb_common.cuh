@@ -130,29 +130,41 @@ struct FusedLayout {
     int fold;          // 0, or the kernel width S when the horizontal taps are folded into
                        // the channels (small C): the kernel then runs fold_geom(g)
     int ts;            // 1: the direct TMEM kernel (K7, conv_ts.cu) serves it (tma = 0)
-    int stack;         // 0, or R*S when the taps are stacked into the output channels: the
-                       // kernel runs stack_geom(g) into a workspace, K9 sums the shifted taps
+    int stack;         // stacked taps (K9 sums the shifted planes): 0 none, 1 all R*S taps
+                       // (kernel: stack_geom(g, 1)), 2 the S horizontal taps (stack_geom(g, 2))
 };
 
-// Tap stacking (few output channels, many input channels): the R*S taps become output
-// channels of a 1x1 conv over the input grid, Y'[n][rs*K + f][h][w] = sum_c x[n][c][h][w] *
-// w[f][c][r][s]; y[n][f][oy][ox] = sum_rs Y'[n][rs*K + f][oy*sh - ph + r*dh][ox*sw - pw +
-// s*dw].  x is read once instead of once per tap.  groups == 1 only.
-inline Geom stack_geom(const Geom& g) {
+// Tap stacking (few output channels, many input channels).  mode 1: all R*S taps become
+// output channels of a 1x1 conv over the input grid, Y'[n][rs*K + f][h][w] = sum_c
+// x[n][c][h][w] * w[f][c][r][s], and y[n][f][oy][ox] = sum_rs Y'[n][rs*K + f][oy*sh - ph +
+// r*dh][ox*sw - pw + s*dw].  mode 2: only the S horizontal taps are stacked -- an R x 1 conv
+// (vertical stride / pad / dilation kept) over all input columns, Y'[n][s*K + f][oy][w], and
+// y[n][f][oy][ox] = sum_s Y'[n][s*K + f][oy][ox*sw - pw + s*dw].  x is read once per
+// remaining tap instead of once per tap, and the MMA N grows by the stacked tap count.
+// groups == 1 only.
+inline Geom stack_geom(const Geom& g, int mode) {
     Geom t = g;
-    t.K = g.R * g.S * g.K;
+    if (mode == 1) {
+        t.K = g.R * g.S * g.K;
+        t.R = 1;
+        t.sh = 1;
+        t.ph = 0;
+        t.dh = 1;
+        t.P = g.H;
+    } else {
+        t.K = g.S * g.K;
+    }
     t.kpg = t.K;
-    t.R = t.S = 1;
-    t.sh = t.sw = 1;
-    t.ph = t.pw = 0;
-    t.dh = t.dw = 1;
-    t.P = g.H;
+    t.S = 1;
+    t.sw = 1;
+    t.pw = 0;
+    t.dw = 1;
     t.Q = g.W;
-    t.PQ = g.HW;
-    t.RS = 1;
-    t.kdim = g.cpg;
+    t.PQ = t.P * t.Q;
+    t.RS = t.R;
+    t.kdim = g.cpg * t.R;
     t.kdim_pad = (t.kdim + 63) / 64 * 64;
-    t.npix = (int64_t)g.N * g.HW;
+    t.npix = (int64_t)g.N * t.PQ;
     return t;
 }
 

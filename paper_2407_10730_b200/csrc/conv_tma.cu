@@ -585,15 +585,25 @@ static FusedLayout base_layout(const Geom& g, bool bf16) {
 // Weights are repacked to match (weight_split_taps, fold) and K0 writes the folded rows.
 bool ts_eligible(const Geom& g);
 
+static int stack_kmax() {  // largest K for row stacking (CB_STACK_KMAX overrides; diagnostics)
+    const char* e = std::getenv("CB_STACK_KMAX");
+    return e ? std::atoi(e) : 32;
+}
+
 FusedLayout fused_layout(const Geom& g, bool bf16) {
     FusedLayout L = base_layout(g, bf16);
     // Few output channels, many input channels: stack the taps (see stack_geom).  The TMA
     // im2col walk would re-read every input pixel once per tap for a handful of MMA columns.
-    if (g.G == 1 && g.RS > 1 && g.RS * g.K <= 256 && g.C >= 128 && !std::getenv("CB_NO_STACK")) {
-        FusedLayout T = base_layout(stack_geom(g), bf16);
-        if (T.tma) {
-            T.stack = g.RS;
-            return T;
+    if (g.G == 1 && g.RS > 1 && !std::getenv("CB_NO_STACK")) {
+        int mode = 0;
+        if (g.RS * g.K <= 256 && g.C >= 128) mode = 1;                          // all taps
+        else if (g.S > 1 && g.S * g.K <= 256 && g.K <= stack_kmax() && g.C >= 64) mode = 2;  // row taps
+        if (mode) {
+            FusedLayout T = base_layout(stack_geom(g, mode), bf16);
+            if (T.tma) {
+                T.stack = mode;
+                return T;
+            }
         }
     }
     // Few channels (C <= 16): the direct kernel builds A in TMEM from TMA-staged fp32 rows

@@ -544,11 +544,16 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
     const int nch = min(WS_CH, cpg - c0);  // real channels in this chunk (may be <= 0)
     // folded (fold = original S, S == 1 here, one chunk): stage all of w[f] in OIHW order
     // and read channel c' = s*C + c of tap r from w[f, c, r, s]
-    // stacked taps (stack_rs > 1, here R = S = 1): row f = rs*K + fo reads w[fo, c, r, s]
+    // stacked taps (stack_rs = T > 1 taps stacked into the rows): row f = t*K + fo, kernel tap
+    // tk reads the original tap tk*T + t of w[fo, c] (all R*S taps: RS = 1; the S horizontal
+    // taps: RS = R, T = S)
     if (stack_rs > 1) {
-        const int fo = f % k_orig, rs = f / k_orig;
-        const float* srcs = w + ((int64_t)fo * cpg + c0) * stack_rs + rs;
-        for (int i = threadIdx.x; i < max(nch, 0); i += 256) ws_tile[i] = __ldg(srcs + (int64_t)i * stack_rs);
+        const int fo = f % k_orig, t = f / k_orig;
+        const float* srcs = w + ((int64_t)fo * cpg + c0) * (RS * stack_rs) + t;
+        for (int i = threadIdx.x; i < max(nch, 0) * RS; i += 256) {
+            const int cl = i / RS, tk = i - cl * RS;
+            ws_tile[i] = __ldg(srcs + ((int64_t)cl * RS + tk) * stack_rs);
+        }
     } else {
         const float* src = w + ((int64_t)f * cpg + c0) * RS;
         for (int i = threadIdx.x; i < max(nch, 0) * RS; i += 256) ws_tile[i] = __ldg(src + i);
@@ -650,13 +655,18 @@ int pre_init_output(const Geom& g, const PixMap& pm, int zero_kind, const float*
 
 namespace cb {
 
-// K9 (stacked taps): y[n][f][oy][ox] = bias[f] + sum_{r,s} Y'[n][(r*S+s)*K + f][iy][ix],
-// iy = oy*sh - ph + r*dh, ix = ox*sw - pw + s*dw (taps outside the image contribute 0),
-// summed in the fixed (r, s) order.  One thread per output, consecutive threads along ox.
+// K9 (stacked taps): y[n][f][oy][ox] = bias[f] + sum over the stacked taps of the shifted
+// planes of Y', in a fixed tap order (deterministic).  mode 1 (all taps, Y' over the input
+// grid): iy = oy*sh - ph + r*dh, ix = ox*sw - pw + s*dw; mode 2 (horizontal taps, Y' over
+// output rows x input columns): row oy, ix as above.  Taps outside the image contribute 0.
+// One thread per output, consecutive threads along ox.
 __global__ void __launch_bounds__(256)
-tap_sum_kernel(Geom g, const float* __restrict__ yp, const float* __restrict__ bias,
+tap_sum_kernel(Geom g, int mode, const float* __restrict__ yp, const float* __restrict__ bias,
                float* __restrict__ y) {
     const int64_t total = (int64_t)g.N * g.K * g.PQ;
+    const int T = mode == 1 ? g.RS : g.S;
+    const int rows = mode == 1 ? g.H : g.P;
+    const int64_t plane = (int64_t)rows * g.W;
     for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (int64_t)gridDim.x * 256) {
         const int64_t nf = i / g.PQ;
         const int pq = (int)(i - nf * g.PQ);
@@ -664,25 +674,28 @@ tap_sum_kernel(Geom g, const float* __restrict__ yp, const float* __restrict__ b
         const int f = (int)(nf - n * g.K);
         const int oy = pq / g.Q, ox = pq - (pq / g.Q) * g.Q;
         float acc = bias ? __ldg(bias + f) : 0.f;
-        const float* base = yp + (n * g.RS * g.K + f) * (int64_t)g.HW;
-        for (int r = 0; r < g.R; ++r) {
-            const int iy = oy * g.sh - g.ph + r * g.dh;
-            if ((unsigned)iy >= (unsigned)g.H) continue;
+        const float* base = yp + (n * T * g.K + f) * plane;
+        const int nr = mode == 1 ? g.R : 1;
+        for (int r = 0; r < nr; ++r) {
+            const int iy = mode == 1 ? oy * g.sh - g.ph + r * g.dh : oy;
+            if ((unsigned)iy >= (unsigned)rows) continue;
             for (int s = 0; s < g.S; ++s) {
                 const int ix = ox * g.sw - g.pw + s * g.dw;
+                const int t = mode == 1 ? r * g.S + s : s;
                 if ((unsigned)ix < (unsigned)g.W)
-                    acc += __ldg(base + (int64_t)(r * g.S + s) * g.K * g.HW + iy * g.W + ix);
+                    acc += __ldg(base + (int64_t)t * g.K * plane + (int64_t)iy * g.W + ix);
             }
         }
         y[i] = acc;
     }
 }
 
-int launch_tap_sum(const Geom& g, const float* yp, const float* bias, float* y, cudaStream_t st) {
+int launch_tap_sum(const Geom& g, int mode, const float* yp, const float* bias, float* y,
+                   cudaStream_t st) {
     const int64_t total = (int64_t)g.N * g.K * g.PQ;
     if (total == 0) return CB_OK;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32);
-    tap_sum_kernel<<<blocks, 256, 0, st>>>(g, yp, bias, y);
+    tap_sum_kernel<<<blocks, 256, 0, st>>>(g, mode, yp, bias, y);
     return check_launch("tap_sum");
 }
 

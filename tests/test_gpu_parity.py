@@ -247,6 +247,11 @@ STACKED = [  # few output channels, many input channels: the stacked-tap path (f
          stride_w=1, pad_h=2, pad_w=2, dil_h=2, dil_w=2, has_bias=True),
     dict(batch=3, in_channels=160, in_h=9, in_w=11, out_channels=10, k_h=1, k_w=7, stride_h=1,
          stride_w=2, pad_h=0, pad_w=3),
+    # row stacking (S*K <= 256 < R*S*K): only the horizontal taps are stacked
+    dict(batch=1, in_channels=64, in_h=19, in_w=21, out_channels=32, k_h=7, k_w=7, stride_h=1,
+         stride_w=1, pad_h=3, pad_w=3, has_bias=True),
+    dict(batch=2, in_channels=96, in_h=16, in_w=18, out_channels=24, k_h=5, k_w=5, stride_h=2,
+         stride_w=2, pad_h=2, pad_w=1, dil_h=1, dil_w=2),
 ]
 
 
