@@ -60,6 +60,8 @@ struct TmaParams {
     int kb_per_split;
     int64_t total_tiles;  // n_tiles * m_tiles * G * splits
     int add_mode;         // 0: store acc + bias, 1: fp32 reduction into out
+    int tma_store;        // 1: epilogue stages 32-channel chunks in smem, TMA-stores y (tm_y)
+    int bulk_parts;       // 1: tail parts write their partial chunks with 1-D bulk copies
     // Tail split-K ("stream-K lite"): the first full_items work items are whole tiles;
     // the tail_tiles tiles of the last, partial wave are each cut into tail_parts K
     // ranges of tail_kbp stages so every cluster gets work.  Parts write fp32 partials to
@@ -94,7 +96,8 @@ struct TmaCfg {
     static constexpr int A_BYTES = TMA_BM * 128;     // one of A_hi / A_lo
     static constexpr int B_BYTES = B_ROWS * 128;     // one of B_hi / B_lo
     static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int OSTAGE_BYTES = 2 * 32 * TMA_BM * 4;  // epilogue: 2 x [32 ch][128 px] fp32
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + OSTAGE_BYTES + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * BN;
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
@@ -156,12 +159,14 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
 conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUtensorMap tm_ahi,
                 const __grid_constant__ CUtensorMap tm_alo,
                 const __grid_constant__ CUtensorMap tm_bhi,
-                const __grid_constant__ CUtensorMap tm_blo) {
+                const __grid_constant__ CUtensorMap tm_blo,
+                const __grid_constant__ CUtensorMap tm_y) {
     using Cfg = TmaCfg<BN, STAGES, BF16, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+    float* ostage = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::OSTAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
@@ -365,6 +370,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
         const uint32_t tempty_leader0 =
             CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0) : 0;
         int local = 0;
+        int ochunk = 0;  // staged output chunks (double-buffered ostage)
         for (int64_t t = cl0; t < p.total_items; t += ncl, ++local) {
             const WorkItem it = decode_item(p, t);
             const int gi = it.gi;
@@ -404,9 +410,27 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                         ptx::tmem_ld_32x32b_x32(
                             tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + c0, r);
                         ptx::tmem_ld_wait();
+                        if (p.bulk_parts) {
+                            // the [32 ch][128 row] chunk is one contiguous 16 KB run of the
+                            // partial slab: stage it, one bulk copy writes it
+                            float* buf = ostage + (ochunk & 1) * (32 * TMA_BM);
+                            if (threadIdx.x == 0) ptx::bulk_wait_read<1>();
+                            epi_barrier();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            __stcg(mine + (int64_t)(c0 + i) * TMA_BM, __uint_as_float(r[i]));
+                            for (int i = 0; i < 32; ++i) buf[i * TMA_BM + row] = __uint_as_float(r[i]);
+                            ptx::fence_proxy_async_smem();
+                            epi_barrier();
+                            if (threadIdx.x == 0) {
+                                ptx::bulk_store_1d(mine - row + (int64_t)c0 * TMA_BM, buf,
+                                                   32 * TMA_BM * 4);
+                                ptx::bulk_commit();
+                            }
+                            ++ochunk;
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                __stcg(mine + (int64_t)(c0 + i) * TMA_BM, __uint_as_float(r[i]));
+                        }
                     }
                     ptx::tc_fence_before();
                     if (CG == 2)
@@ -414,6 +438,10 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                     else
                         ptx::mbar_arrive(&tempty[acc]);
                     if (threadIdx.x == 0) trace_stamp(p, 20);  // partial written (issued)
+                    if (p.bulk_parts && threadIdx.x == 0) {
+                        ptx::bulk_wait_all();  // the bulk writes are performed ...
+                        asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and visible
+                    }
                     __threadfence();
                     epi_barrier();
                     if (threadIdx.x == 0) {
@@ -432,44 +460,88 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 __threadfence();
                 // Add the other parts into the TMEM accumulator (no global stores here, so
                 // the partial loads never queue behind output stores in L1), then fall
-                // through to the ordinary epilogue below.
-#pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
-                    if (f_tile0 + c0 >= g.kpg) break;
-                    const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + c0;
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(taddr, r);
-                    // all parts' loads of this chunk in flight at once (<= MAX_TAIL_OTHERS)
-                    float v[MAX_TAIL_OTHERS][32];
+                // through to the ordinary epilogue below.  16-column steps, software
+                // pipelined: the loads of step h+1 are in flight while step h is added.
+                const int ncols = min(BN, g.kpg - f_tile0);
+                const int nh = (ncols + 15) / 16;
+                auto load_parts = [&](float (&v)[MAX_TAIL_OTHERS][16], int h) {
 #pragma unroll
                     for (int q = 0; q < MAX_TAIL_OTHERS; ++q) {
-                        const float* src = part_base + (int64_t)q * CG * slab + (int64_t)c0 * TMA_BM;
+                        const float* src = part_base + (int64_t)q * CG * slab + (int64_t)(h * 16) * TMA_BM;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
+                        for (int i = 0; i < 16; ++i)
                             v[q][i] = q < others ? __ldcg(src + (int64_t)i * TMA_BM) : 0.f;
                     }
+                };
+                auto add_parts = [&](const float (&v)[MAX_TAIL_OTHERS][16], int h) {
+                    const uint32_t taddr =
+                        tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + h * 16;
+                    uint32_t r[16];
+                    ptx::tmem_ld_32x32b_x16(taddr, r);
                     ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
+                    for (int i = 0; i < 16; ++i) {
                         float s = __uint_as_float(r[i]);
 #pragma unroll
                         for (int q = 0; q < MAX_TAIL_OTHERS; ++q) s += v[q][i];
                         r[i] = __float_as_uint(s);
                     }
-                    ptx::tmem_st_32x32b_x32(taddr, r);
+                    ptx::tmem_st_32x32b_x16(taddr, r);
+                };
+                float va[MAX_TAIL_OTHERS][16], vb[MAX_TAIL_OTHERS][16];
+                if (nh > 0) load_parts(va, 0);
+#pragma unroll 1
+                for (int h = 0; h < nh; h += 2) {
+                    if (h + 1 < nh) load_parts(vb, h + 1);
+                    add_parts(va, h);
+                    if (h + 2 < nh) load_parts(va, h + 2);
+                    if (h + 1 < nh) add_parts(vb, h + 1);
                 }
+                if (threadIdx.x == 0) trace_stamp(p, 24);  // partials added
                 ptx::tmem_st_wait();
             }
 
+            const int nchunk = (min(BN, g.kpg - f_tile0) + 31) / 32;
+            // TMA store only for tiles inside one image (a box may not start at a negative
+            // pixel coordinate); tiles across an image boundary store directly
+            const int64_t m0t = it.mt * (TMA_BM * CG) + rank * TMA_BM;
+            const int64_t n0t = m0t / g.PQ;
+            const bool tile_tstore =
+                p.tma_store && m0t < g.npix && (min(m0t + TMA_BM, g.npix) - 1) / g.PQ == n0t;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int ci = 0; ci < nchunk; ++ci) {
+                const int c0 = ci * 32;
                 const int nvalid = min(32, g.kpg - (f_tile0 + c0));  // warp-uniform
-                if (nvalid <= 0) break;
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + c0,
                                         r);
                 ptx::tmem_ld_wait();
-                if (do_store) {
+                if (ci + 1 == nchunk) {  // the whole accumulator is in registers: release it
+                    ptx::tc_fence_before();
+                    if (CG == 2)
+                        ptx::mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
+                    else
+                        ptx::mbar_arrive(&tempty[acc]);
+                }
+                if (tile_tstore && !(p.debug & 2)) {
+                    // stage [32 ch][128 px] (+bias) and TMA-store it (the tensor map clips
+                    // the image's last tile)
+                    float* buf = ostage + (ochunk & 1) * (32 * TMA_BM);
+                    if (threadIdx.x == 0) ptx::bulk_wait_read<1>();
+                    epi_barrier();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        buf[i * TMA_BM + row] = __uint_as_float(r[i]) +
+                                                (bias && i < nvalid ? __ldg(bias + c0 + i) : 0.f);
+                    ptx::fence_proxy_async_smem();
+                    epi_barrier();
+                    if (threadIdx.x == 0) {
+                        ptx::tma_store_3d(&tm_y, buf, (int32_t)(m0t - n0t * g.PQ),
+                                          gi * g.kpg + f_tile0 + c0, (int32_t)n0t);
+                        ptx::bulk_commit();
+                    }
+                    ++ochunk;
+                } else if (do_store) {
                     if (p.add_mode) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -487,13 +559,11 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 }
                 dst += (int64_t)32 * g.PQ;
             }
-            ptx::tc_fence_before();
-            if (CG == 2)
-                ptx::mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-            else
-                ptx::mbar_arrive(&tempty[acc]);
         }
-        if (threadIdx.x == 0) trace_stamp(p, TRACE_SLOTS - 1);  // epilogue finished
+        if (threadIdx.x == 0) {
+            ptx::bulk_wait_all();  // smem sources must outlive the bulk stores
+            trace_stamp(p, TRACE_SLOTS - 1);  // epilogue finished
+        }
     }
 
     ptx::tc_fence_before();
@@ -690,7 +760,7 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     pl.splits = (L.num_kb + pl.kb_per_split - 1) / pl.kb_per_split;
     pl.total_tiles = tiles * pl.splits;
     const int stage_bytes = 2 * TMA_BM * 128 + 2 * (pl.bn / pl.cg) * 128;
-    pl.stages = std::min(6, (232448 - 1280) / stage_bytes);
+    pl.stages = std::min(6, (232448 - 1280 - 2 * 32 * TMA_BM * 4) / stage_bytes);  // - epilogue stage
     // Tail split-K: when whole tiles leave the last wave partly idle -- or a single short
     // wave leaves clusters idle -- cut each tail tile into S K-parts so the last wave fills
     // more clusters.  Parts keep >= 4 K-blocks when the grid is over-full (the fixup must
@@ -811,12 +881,24 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     });
     if (attr_err != cudaSuccess)
         return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-    CUtensorMap mah, mal, mwh, mwl;
+    CUtensorMap mah, mal, mwh, mwl, my{};
     int rc;
     if ((rc = make_act_map(&mah, BF16, prm.g, prm.L, ahi))) return rc;
     if ((rc = make_act_map(&mal, BF16, prm.g, prm.L, alo))) return rc;
     if ((rc = make_w_map(&mwh, BF16, whi, prm.g.K, prm.L.kw_pad, Cfg::B_ROWS))) return rc;
     if ((rc = make_w_map(&mwl, BF16, wlo, prm.g.K, prm.L.kw_pad, Cfg::B_ROWS))) return rc;
+    if (prm.tma_store) {  // y as {PQ, K, N}, boxes of 128 pixels x 32 channels
+        auto fn = tiled_encode_fn();
+        cuuint64_t dims[3] = {(cuuint64_t)prm.g.PQ, (cuuint64_t)prm.g.K, (cuuint64_t)prm.g.N};
+        cuuint64_t strides[2] = {(cuuint64_t)prm.g.PQ * 4, (cuuint64_t)prm.g.K * prm.g.PQ * 4};
+        cuuint32_t box[3] = {(cuuint32_t)TMA_BM, 32, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = fn(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, prm.out, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string((int)r));
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(TMA_THREADS);
@@ -829,7 +911,7 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mah, mal, mwh, mwl);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mah, mal, mwh, mwl, my);
     if (e != cudaSuccess) return fail(CB_ERR_CUDA, std::string("conv_tma launch: ") + cudaGetErrorString(e));
     return check_launch("conv_tma_kernel");
 }
@@ -887,11 +969,19 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     }
     prm.add_mode = 0;
     if (const char* dbg = std::getenv("CB_TMA_DEBUG")) prm.debug = std::atoi(dbg);
+    // Optional TMA-store epilogue (CB_TMA_TSTORE) and bulk-copy tail partials
+    // (CB_TMA_BULK_PARTS): measured equal or slower than the direct stores on cfg4 and on
+    // output-heavy sweep ops (two epilogue barriers per chunk; tiles crossing images fall
+    // back to direct stores anyway), so both are off by default.
+    prm.tma_store = (g.PQ % 4 == 0) && (g.G == 1 || g.kpg % 32 == 0) &&
+                    (reinterpret_cast<uintptr_t>(y) & 15) == 0 && std::getenv("CB_TMA_TSTORE");
+    prm.bulk_parts = std::getenv("CB_TMA_BULK_PARTS") ? 1 : 0;
     if (std::getenv("CB_TMA_TRACE")) prm.trace = debug_trace_buffer(pl.grid, st);
     if (pl.splits > 1) {
         int rc = launch_fill_bias(g.N, g.K, g.PQ, bias, y, st);
         if (rc) return rc;
         prm.add_mode = 1;
+        prm.tma_store = 0;
     }
 #define CB_TMA_CASE(CG_, BN_, ST_)                                                               \
     if (pl.cg == CG_ && pl.bn == BN_ && pl.stages == ST_)                                         \

@@ -55,7 +55,7 @@ def main(name="cfg4", variant="tc3xbf16"):
               f"max {np.nanmax(col):7.1f} us  (ctas {int(np.sum(~np.isnan(col)))})")
     print(f"  epilogue-done   min {np.nanmin(ends):7.1f} med {np.nanmedian(ends):7.1f} max {np.nanmax(ends):7.1f} us")
     for s, label in ((20, "part written"), (21, "part published"), (22, "owner waits"),
-                     (23, "owner released")):
+                     (23, "owner released"), (24, "partials added")):
         col = rel[:, s]
         if not np.all(np.isnan(col)):
             print(f"  {label:15s} min {np.nanmin(col):7.1f} med {np.nanmedian(col):7.1f} "
