@@ -70,8 +70,8 @@ struct TmaParams {
     int64_t full_items;
     int tail_tiles, tail_parts, tail_kbp;
     int64_t total_items;
-    int* counters;        // tail_tiles * CG, zeroed by K0 before every launch
-    float* partials;      // tail_tiles * (tail_parts - 1) * CG * BN * 128
+    int* counters;        // 2 * tail_tiles * CG ([written][done]), self-resetting
+    float* partials;      // tail_tiles * tail_parts * CG * BN * 128
     unsigned long long* trace;  // diagnostics (CB_TMA_TRACE): per-CTA globaltimer stamps
     int debug;            // diagnostics only (CB_TMA_DEBUG): 1 = skip operand loads,
                           // 2 = skip epilogue stores, 3 = both.  Results are garbage.
@@ -393,112 +393,89 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
             const float* bias = p.bias ? p.bias + gi * g.kpg + f_tile0 : nullptr;
 
             if (it.tail >= 0) {
-                // ---- tail split-K: parts 1.. park fp32 partials ([channel][row]: every warp
-                // access is one 128-byte line); part 0 owns the tile, keeps its accumulator
-                // in TMEM, waits for the others (all tail parts run concurrently in the last
-                // wave on distinct, co-resident clusters), adds their partials in part order
-                // and stores. ----
+                // ---- tail split-K, symmetric fixup: the P parts of a tail tile run
+                // concurrently on distinct co-resident clusters; part p owns the 32-channel
+                // chunks [P*p/.., ..) of the tile.  Every part parks the chunks it does not
+                // own as fp32 partials ([channel][row]: each warp access one 128-byte line),
+                // publishes, waits for all P, then sums its own chunks over the parts in part
+                // order (deterministic) and stores them.  Counters: [written][done] per
+                // (tail tile, CTA rank); the last part through `done` resets both. ----
+                const int P = p.tail_parts;
                 const int64_t slab = (int64_t)BN * TMA_BM;
-                const int others = p.tail_parts - 1;
-                float* part_base = p.partials + ((int64_t)it.tail * others * CG + rank) * slab + row;
-                int* ctr = p.counters + it.tail * CG + rank;
-                if (it.part > 0) {
-                    float* mine = part_base + (int64_t)(it.part - 1) * CG * slab;
+                const int nch = (min(BN, g.kpg - f_tile0) + 31) / 32;
+                const int own_lo = it.part * nch / P, own_hi = (it.part + 1) * nch / P;
+                float* slab_of = p.partials + ((int64_t)it.tail * P * CG + rank) * slab + row;  // + q*CG*slab
+                int* written = p.counters + 2 * (it.tail * CG + rank);
+                int* done = written + 1;
+                const uint32_t lane_tm = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
+                float* mine = slab_of + (int64_t)it.part * CG * slab;
 #pragma unroll 1
-                    for (int c0 = 0; c0 < BN; c0 += 32) {
-                        uint32_t r[32];
-                        ptx::tmem_ld_32x32b_x32(
-                            tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + c0, r);
-                        ptx::tmem_ld_wait();
-                        if (p.bulk_parts) {
-                            // the [32 ch][128 row] chunk is one contiguous 16 KB run of the
-                            // partial slab: stage it, one bulk copy writes it
-                            float* buf = ostage + (ochunk & 1) * (32 * TMA_BM);
-                            if (threadIdx.x == 0) ptx::bulk_wait_read<1>();
-                            epi_barrier();
+                for (int ci = 0; ci < nch; ++ci) {
+                    if (ci >= own_lo && ci < own_hi) continue;
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(lane_tm + ci * 32, r);
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) buf[i * TMA_BM + row] = __uint_as_float(r[i]);
-                            ptx::fence_proxy_async_smem();
-                            epi_barrier();
-                            if (threadIdx.x == 0) {
-                                ptx::bulk_store_1d(mine - row + (int64_t)c0 * TMA_BM, buf,
-                                                   32 * TMA_BM * 4);
-                                ptx::bulk_commit();
-                            }
-                            ++ochunk;
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                __stcg(mine + (int64_t)(c0 + i) * TMA_BM, __uint_as_float(r[i]));
-                        }
-                    }
-                    ptx::tc_fence_before();
-                    if (CG == 2)
-                        ptx::mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-                    else
-                        ptx::mbar_arrive(&tempty[acc]);
-                    if (threadIdx.x == 0) trace_stamp(p, 20);  // partial written (issued)
-                    if (p.bulk_parts && threadIdx.x == 0) {
-                        ptx::bulk_wait_all();  // the bulk writes are performed ...
-                        asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and visible
-                    }
-                    __threadfence();
-                    epi_barrier();
-                    if (threadIdx.x == 0) {
-                        atomicAdd(ctr, 1);
-                        trace_stamp(p, 21);  // partial published
-                    }
-                    continue;
+                    for (int i = 0; i < 32; ++i)
+                        __stcg(mine + (int64_t)(ci * 32 + i) * TMA_BM, __uint_as_float(r[i]));
                 }
+                if (threadIdx.x == 0) trace_stamp(p, 20);  // partials written (issued)
+                __threadfence();
+                epi_barrier();
                 if (threadIdx.x == 0) {
-                    trace_stamp(p, 22);  // owner starts waiting
-                    while (*reinterpret_cast<volatile int*>(ctr) < others) __nanosleep(128);
-                    *ctr = 0;  // every other part has arrived: ready for the next launch
-                    trace_stamp(p, 23);  // owner released
+                    atomicAdd(written, 1);
+                    trace_stamp(p, 22);  // waiting for the other parts
+                    while (*reinterpret_cast<volatile int*>(written) < P) __nanosleep(64);
+                    trace_stamp(p, 23);  // all parts published
                 }
                 epi_barrier();
                 __threadfence();
-                // Add the other parts into the TMEM accumulator (no global stores here, so
-                // the partial loads never queue behind output stores in L1), then fall
-                // through to the ordinary epilogue below.  16-column steps, software
-                // pipelined: the loads of step h+1 are in flight while step h is added.
-                const int ncols = min(BN, g.kpg - f_tile0);
-                const int nh = (ncols + 15) / 16;
-                auto load_parts = [&](float (&v)[MAX_TAIL_OTHERS][16], int h) {
-#pragma unroll
-                    for (int q = 0; q < MAX_TAIL_OTHERS; ++q) {
-                        const float* src = part_base + (int64_t)q * CG * slab + (int64_t)(h * 16) * TMA_BM;
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            v[q][i] = q < others ? __ldcg(src + (int64_t)i * TMA_BM) : 0.f;
-                    }
-                };
-                auto add_parts = [&](const float (&v)[MAX_TAIL_OTHERS][16], int h) {
-                    const uint32_t taddr =
-                        tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + h * 16;
-                    uint32_t r[16];
-                    ptx::tmem_ld_32x32b_x16(taddr, r);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float s = __uint_as_float(r[i]);
-#pragma unroll
-                        for (int q = 0; q < MAX_TAIL_OTHERS; ++q) s += v[q][i];
-                        r[i] = __float_as_uint(s);
-                    }
-                    ptx::tmem_st_32x32b_x16(taddr, r);
-                };
-                float va[MAX_TAIL_OTHERS][16], vb[MAX_TAIL_OTHERS][16];
-                if (nh > 0) load_parts(va, 0);
+                // own chunks: all other parts' values of a chunk are loaded before any of its
+                // stores issue (loads never queue behind stores in L1)
 #pragma unroll 1
-                for (int h = 0; h < nh; h += 2) {
-                    if (h + 1 < nh) load_parts(vb, h + 1);
-                    add_parts(va, h);
-                    if (h + 2 < nh) load_parts(va, h + 2);
-                    if (h + 1 < nh) add_parts(vb, h + 1);
+                for (int ci = own_lo; ci < own_hi; ++ci) {
+                    const int c0 = ci * 32;
+                    const int nvalid = min(32, g.kpg - (f_tile0 + c0));
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(lane_tm + c0, r);
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                    for (int q = 0; q < P; ++q) {  // sum over parts in part order
+                        if (q == it.part) {
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
+                        } else {
+                            const float* src = slab_of + (int64_t)q * CG * slab + (int64_t)c0 * TMA_BM;
+                            float pv[32];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) pv[i] = __ldcg(src + (int64_t)i * TMA_BM);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] += pv[i];
+                        }
+                    }
+                    if (do_store) {
+                        float* d = dst + (int64_t)c0 * g.PQ;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < nvalid)
+                                d[(int64_t)i * g.PQ] = v[i] + (bias ? __ldg(bias + c0 + i) : 0.f);
+                    }
                 }
-                if (threadIdx.x == 0) trace_stamp(p, 24);  // partials added
-                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                if (CG == 2)
+                    ptx::mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
+                else
+                    ptx::mbar_arrive(&tempty[acc]);
+                if (threadIdx.x == 0) {
+                    trace_stamp(p, 24);  // own chunks stored
+                    if (atomicAdd(done, 1) == P - 1) {  // every part is past its wait
+                        *written = 0;
+                        *done = 0;
+                    }
+                }
+                continue;
             }
 
             const int nchunk = (min(BN, g.kpg - f_tile0) + 31) / 32;
@@ -799,13 +776,13 @@ int64_t tma_tail_workspace_bytes(const Geom& g, const FusedLayout& L) {
     if (!L.tma || g.npix == 0) return 0;
     TmaPlan pl = plan_tma(g, L);
     if (pl.tail_tiles == 0) return 0;
-    const int64_t ctr = ((int64_t)pl.tail_tiles * pl.cg * 4 + 255) / 256 * 256;
-    return ctr + (int64_t)pl.tail_tiles * (pl.tail_parts - 1) * pl.cg * pl.bn * TMA_BM * 4;
+    const int64_t ctr = ((int64_t)pl.tail_tiles * pl.cg * 8 + 255) / 256 * 256;  // [written][done]
+    return ctr + (int64_t)pl.tail_tiles * pl.tail_parts * pl.cg * pl.bn * TMA_BM * 4;
 }
 int tma_tail_counters(const Geom& g, const FusedLayout& L) {
     if (!L.tma || g.npix == 0) return 0;
     TmaPlan pl = plan_tma(g, L);
-    return pl.tail_tiles * pl.cg;
+    return 2 * pl.tail_tiles * pl.cg;
 }
 
 int tma_plan_query(const Geom& g, bool bf16, cb_tile_plan* out) {
@@ -963,7 +940,7 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     prm.tail_kbp = pl.tail_kbp;
     if (pl.tail_tiles > 0) {
         if (!tail_ws) return fail(CB_ERR_WORKSPACE, "tail split-K needs workspace");
-        const int64_t ctr = ((int64_t)pl.tail_tiles * pl.cg * 4 + 255) / 256 * 256;
+        const int64_t ctr = ((int64_t)pl.tail_tiles * pl.cg * 8 + 255) / 256 * 256;
         prm.counters = static_cast<int*>(tail_ws);
         prm.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(tail_ws) + ctr);
     }
