@@ -404,7 +404,9 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 const int64_t slab = (int64_t)BN * TMA_BM;
                 const int nch = (min(BN, g.kpg - f_tile0) + 31) / 32;
                 const int own_lo = it.part * nch / P, own_hi = (it.part + 1) * nch / P;
-                float* slab_of = p.partials + ((int64_t)it.tail * P * CG + rank) * slab + row;  // + q*CG*slab
+                // partial slab layout [ch / 4][row][ch % 4]: a thread's 4 consecutive channels
+                // are one float4 and a warp's float4 accesses are one 512-byte run
+                float* slab_of = p.partials + ((int64_t)it.tail * P * CG + rank) * slab;  // + q*CG*slab
                 int* written = p.counters + 2 * (it.tail * CG + rank);
                 int* done = written + 1;
                 const uint32_t lane_tm = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
@@ -416,8 +418,10 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                     ptx::tmem_ld_32x32b_x32(lane_tm + ci * 32, r);
                     ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        __stcg(mine + (int64_t)(ci * 32 + i) * TMA_BM, __uint_as_float(r[i]));
+                    for (int j = 0; j < 8; ++j)
+                        __stcg(reinterpret_cast<float4*>(mine) + (int64_t)(ci * 8 + j) * TMA_BM + row,
+                               make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                           __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
                 }
                 if (threadIdx.x == 0) trace_stamp(p, 20);  // partials written (issued)
                 __threadfence();
@@ -447,12 +451,19 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
                         } else {
-                            const float* src = slab_of + (int64_t)q * CG * slab + (int64_t)c0 * TMA_BM;
-                            float pv[32];
+                            const float4* src = reinterpret_cast<const float4*>(
+                                                    slab_of + (int64_t)q * CG * slab) +
+                                                (int64_t)(ci * 8) * TMA_BM + row;
+                            float4 pv[8];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) pv[i] = __ldcg(src + (int64_t)i * TMA_BM);
+                            for (int j = 0; j < 8; ++j) pv[j] = __ldcg(src + (int64_t)j * TMA_BM);
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) v[i] += pv[i];
+                            for (int j = 0; j < 8; ++j) {
+                                v[4 * j] += pv[j].x;
+                                v[4 * j + 1] += pv[j].y;
+                                v[4 * j + 2] += pv[j].z;
+                                v[4 * j + 3] += pv[j].w;
+                            }
                         }
                     }
                     if (do_store) {
