@@ -210,6 +210,9 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
         __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // everything above overlapped the preceding kernel; its outputs (the split activations,
+    // the zeroed tail counters) are read only after this point
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == PRODUCER_WARP) {
         // ================================ TMA producer ==================================
@@ -892,13 +895,17 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     cfg.blockDim = dim3(TMA_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: the prologue (barriers, TMEM, descriptor prefetch)
+    // overlaps the tail of the preceding kernel (K0); griddepcontrol.wait guards the inputs
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = std::getenv("CB_NO_PDL") ? 0 : 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mah, mal, mwh, mwl, my);
     if (e != cudaSuccess) return fail(CB_ERR_CUDA, std::string("conv_tma launch: ") + cudaGetErrorString(e));
     return check_launch("conv_tma_kernel");

@@ -460,6 +460,8 @@ act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
                       int n_counters) {
     constexpr int VEC = BF16 ? 8 : 4;
     __shared__ float tile[64][33];
+    // let the dependent conv kernel (PDL) launch and run its prologue early
+    asm volatile("griddepcontrol.launch_dependents;");
     // the fused conv's tail split-K counters start every launch at zero
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
         for (int i = threadIdx.x; i < n_counters; i += 256) counters[i] = 0;
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(256)
 act_fold_split_kernel(Geom g, int c_alloc, const float* __restrict__ x, void* __restrict__ hi_out,
                       void* __restrict__ lo_out, int* counters, int n_counters) {
     constexpr int VEC = BF16 ? 8 : 4;
+    asm volatile("griddepcontrol.launch_dependents;");
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < n_counters; i += 256) counters[i] = 0;
     const int nq = c_alloc / VEC;
