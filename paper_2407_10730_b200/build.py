@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libconvb200.so"
-SOURCES = ["capi.cu", "pack_kernels.cu", "conv_tc.cu", "conv_tma.cu", "conv_ts.cu", "conv_ffma.cu"]
+SOURCES = ["capi.cu", "pack_kernels.cu", "conv_tc.cu", "conv_tma.cu", "conv_ts.cu", "conv_gemm_ts.cu", "conv_ffma.cu"]
 HEADERS = ["cb_common.cuh", "sm100_ptx.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -131,6 +131,9 @@ int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, cons
 int launch_ffma(const Geom& g, const PixMap& pm, const float* src, const float* w,
                 const float* bias, float* out, int add_mode, int zero_kind, cudaStream_t st);
 
+int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
+                   const void* w_lo, const float* bias, float* out, int add_mode, cudaStream_t st);
+
 static int run_variant(int variant, const Geom& g, const PixMap& pm, const float* src,
                        const void* w_hi, const void* w_lo, const float* w_f32, const float* bias,
                        float* out, int add_mode, int zero_kind, cudaStream_t st) {
@@ -138,6 +141,11 @@ static int run_variant(int variant, const Geom& g, const PixMap& pm, const float
         case CB_VARIANT_TC3XTF32:
         case CB_VARIANT_TC3XBF16:
             if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need split weights");
+            {  // K8 (A in TMEM) for the matrix / slice GEMMs; K4 otherwise
+                const int rc = launch_gemm_ts(variant == CB_VARIANT_TC3XBF16, g, pm, src, w_hi,
+                                              w_lo, bias, out, add_mode, st);
+                if (rc != CB_ERR_UNSUPPORTED) return rc;
+            }
             return launch_tc(variant == CB_VARIANT_TC3XBF16, g, pm, src, w_hi, w_lo, bias, out,
                              add_mode, zero_kind, st);
         case CB_VARIANT_FFMA:

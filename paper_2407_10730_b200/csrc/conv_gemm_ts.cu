@@ -1,0 +1,475 @@
+// conv_gemm_ts.cu -- K8: the stepwise algorithms' GEMM microkernel (im2col matrix or SConv
+// slice buffer x split weights) on tcgen05 with the A operand built in TMEM.
+//
+// K4 (conv_tc.cu) gathers its fp32 operand per thread into a swizzled smem tile, one tile
+// per CTA (not persistent, wave-quantized).  K8 instead:
+//
+//   * warps 0-7 (producers, two per TMEM lane quadrant, alternating 32-wide K chunks) read
+//     the fp32 operand rows -- pixel j, reduction k at base(j) + k*stride(j), coalesced along
+//     pixels -- split each value (bf16 or tf32 hi/lo) and write the chunk straight into a
+//     TMEM ring with tcgen05.st;
+//   * warp 12 TMA-streams the split weight tiles (K-major, SWIZZLE_128B) through an smem ring;
+//   * warp 13 issues A_lo*B_hi, A_hi*B_lo, A_hi*B_hi per K step with A read from TMEM;
+//   * warps 8-11 drain the accumulator through the PixMap output modes (NCHW + bias, SConv
+//     slice accumulators, or a row-major matrix, optionally accumulating into it).
+//
+// Persistent: one CTA per SM walks (pixel tile, channel tile, group) items.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "cb_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace cb {
+
+constexpr int G8_BM = 128;
+constexpr int G8_PROD_WARPS = 8;
+constexpr int G8_EPI_WARP0 = 8;
+constexpr int G8_TMA_WARP = 12;
+constexpr int G8_MMA_WARP = 13;
+constexpr int G8_ATMA_WARP = 14;  // A tiles by TMA (matrix sources)
+constexpr int G8_THREADS = 15 * 32;
+constexpr int G8_ASTAGES = 4;
+constexpr int G8_ASTAGE_BYTES = 32 * G8_BM * 4;  // [32 k][128 px] fp32
+constexpr int G8_TMEM_COLS = 512;
+constexpr int G8_CK = 32;  // reduction elements per A chunk
+
+struct G8Params {
+    Geom g;
+    PixMap pm;
+    const float* src;
+    const float* bias;
+    float* out;
+    int add_mode;     // 1: out += acc (no bias), 0: out = acc (+bias)
+    int n_tiles;      // channel tiles per group
+    int64_t m_tiles;  // pixel tiles
+    int64_t items;    // m_tiles * n_tiles * G
+    int nchunks;      // ceil(kdim / 32)
+    int ring;         // A chunks in the TMEM ring
+    int bstages;      // smem weight stages
+    int tma_a;        // 1: A chunks arrive by TMA into smem, 0: per-thread loads
+    int tps;          // > 0: SConv slices, tiles never cross a slice: tps tiles per slice of np px
+    int np;
+};
+
+template <int BN, bool BF16>
+struct G8Cfg {
+    static constexpr int EB = BF16 ? 2 : 4;
+    static constexpr int KE = 128 / EB;            // reduction per weight stage (128-byte rows)
+    static constexpr int CPS = KE / G8_CK;         // A chunks per weight stage: 2 (bf16), 1 (tf32)
+    static constexpr int UK = 32 / EB;             // reduction per MMA
+    static constexpr int HALF_COLS = G8_CK * EB / 4;  // TMEM columns of one half of a chunk
+    static constexpr int CHUNK_COLS = 2 * HALF_COLS;
+    static constexpr int B_BYTES = BN * 128;       // one half (hi or lo) of a weight stage
+    static constexpr int STAGE_BYTES = 2 * B_BYTES;
+};
+
+template <int BN, bool BF16>
+__global__ void __launch_bounds__(G8_THREADS, 1)
+gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUtensorMap tm_hi,
+               const __grid_constant__ CUtensorMap tm_lo, const __grid_constant__ CUtensorMap tm_a) {
+    using Cfg = G8Cfg<BN, BF16>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    float* astage = reinterpret_cast<float*>(smem + p.bstages * Cfg::STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bstages * Cfg::STAGE_BYTES +
+                                                 G8_ASTAGES * G8_ASTAGE_BYTES);
+    uint64_t* b_full = bars;                    // [bstages]
+    uint64_t* b_empty = b_full + p.bstages;     // [bstages]
+    uint64_t* a_full = b_empty + p.bstages;     // [ring]
+    uint64_t* a_empty = a_full + p.ring;        // [ring]
+    uint64_t* acc_full = a_empty + p.ring;      // 1
+    uint64_t* acc_empty = acc_full + 1;         // 1
+    uint64_t* as_full = acc_empty + 1;          // [G8_ASTAGES]
+    uint64_t* as_empty = as_full + G8_ASTAGES;  // [G8_ASTAGES]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(as_empty + G8_ASTAGES);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const Geom& g = p.g;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.bstages; ++s) {
+            ptx::mbar_init(&b_full[s], 1);
+            ptx::mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < p.ring; ++s) {
+            ptx::mbar_init(&a_full[s], 128);
+            ptx::mbar_init(&a_empty[s], 1);
+        }
+        ptx::mbar_init(acc_full, 1);
+        ptx::mbar_init(acc_empty, 128);
+        for (int s = 0; s < G8_ASTAGES; ++s) {
+            ptx::mbar_init(&as_full[s], 1);
+            ptx::mbar_init(&as_empty[s], 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == G8_TMA_WARP && lane == 0) {
+        ptx::tma_prefetch_desc(&tm_hi);
+        ptx::tma_prefetch_desc(&tm_lo);
+    }
+    if (warp == G8_MMA_WARP) ptx::tmem_alloc(tmem_slot, G8_TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int nch = p.nchunks;
+
+    // pixel tile mt, row m -> launch-local pixel jl (slice-aligned tiles for slice sources)
+    auto pix_of = [&](int64_t mt, int m, int64_t& jl) -> bool {
+        if (p.tps) {
+            const int64_t sl = mt / p.tps;
+            const int off = (int)(mt - sl * p.tps) * G8_BM + m;
+            jl = sl * p.np + off;
+            return off < p.np;
+        }
+        jl = mt * G8_BM + m;
+        return jl < p.pm.j_count;
+    };
+    // item -> (channel tile nt, pixel tile mt, group gi)
+    auto decode = [&](int64_t t, int& nt, int64_t& mt, int& gi) {
+        nt = (int)(t % p.n_tiles);
+        const int64_t r = t / p.n_tiles;
+        mt = r % p.m_tiles;
+        gi = (int)(r / p.m_tiles);
+    };
+
+    if (warp < G8_PROD_WARPS) {
+        // ============================ A producers ======================================
+        const int quad = warp & 3, kpar = warp >> 2;
+        const int m = quad * 32 + lane;
+        const uint32_t lane_tm = tmem_base + ((uint32_t)(quad * 32) << 16) + BN;  // ring base
+        int64_t cbase = 0;  // chunks this CTA produced before the current item
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch) {
+            int nt, gi;
+            int64_t mt;
+            decode(t, nt, mt, gi);
+            int64_t jl;
+            const bool jvalid = pix_of(mt, m, jl);
+            int64_t lbase = 0, lstride = 0;
+            if (jvalid) src_linear(g, p.pm, p.pm.j_begin + jl, lbase, lstride);
+            const int64_t row0 = p.pm.src_mode == SRC_MATRIX ? (int64_t)gi * g.kdim : 0;
+            const float* srcp = p.src + lbase + row0 * lstride;
+            for (int kc = kpar; kc < nch; kc += 2) {
+                const int64_t cg = cbase + kc;
+                const int slot = (int)(cg % p.ring);
+                const uint32_t ph = (uint32_t)((cg / p.ring) & 1);
+                float v[G8_CK];
+                const int k0 = kc * G8_CK;
+                if (p.tma_a) {  // the chunk's [32 k][128 px] box is in smem: read column m
+                    const int as = (int)(cg % G8_ASTAGES);
+                    ptx::mbar_wait(&as_full[as], (uint32_t)((cg / G8_ASTAGES) & 1));
+                    const float* col = astage + (size_t)as * (32 * G8_BM) + m;
+#pragma unroll
+                    for (int e = 0; e < G8_CK; ++e) v[e] = col[e * G8_BM];
+                    ptx::mbar_arrive(&as_empty[as]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < G8_CK; ++e)
+                        v[e] = (jvalid && k0 + e < g.kdim) ? __ldg(srcp + (int64_t)(k0 + e) * lstride) : 0.f;
+                }
+                ptx::mbar_wait(&a_empty[slot], ph ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t a_hi = lane_tm + slot * Cfg::CHUNK_COLS;
+                const uint32_t a_lo = a_hi + Cfg::HALF_COLS;
+                if (BF16) {
+                    uint32_t hv[16], lv[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const uint16_t h0 = bf16_rn_bits(v[2 * e]), h1 = bf16_rn_bits(v[2 * e + 1]);
+                        const uint16_t l0 = bf16_rn_bits(v[2 * e] - bf16_bits_to_f32(h0));
+                        const uint16_t l1 = bf16_rn_bits(v[2 * e + 1] - bf16_bits_to_f32(h1));
+                        hv[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+                        lv[e] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+                    }
+                    ptx::tmem_st_32x32b_x16(a_hi, hv);
+                    ptx::tmem_st_32x32b_x16(a_lo, lv);
+                } else {
+                    uint32_t hv[32], lv[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const Split2 sp = split_tf32(v[e]);
+                        hv[e] = __float_as_uint(sp.hi);
+                        lv[e] = __float_as_uint(sp.lo);
+                    }
+                    ptx::tmem_st_32x32b_x32(a_hi, hv);
+                    ptx::tmem_st_32x32b_x32(a_lo, lv);
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&a_full[slot]);
+            }
+        }
+    } else if (warp < G8_TMA_WARP) {
+        // ============================ epilogue ==========================================
+        const int quad = warp & 3;
+        const int m = quad * 32 + lane;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++i) {
+            int nt, gi;
+            int64_t mt;
+            decode(t, nt, mt, gi);
+            int64_t jl;
+            const bool jvalid = pix_of(mt, m, jl);
+            int64_t obase = 0, ostride = 0;
+            if (jvalid) dst_linear(g, p.pm, p.pm.j_begin + jl, obase, ostride);
+            const int f_tile0 = nt * BN;
+            ptx::mbar_wait(acc_full, i & 1);
+            ptx::tc_fence_after();
+            const int ncol = min(BN, g.kpg - f_tile0);
+#pragma unroll 1
+            for (int c0 = 0; c0 < ncol; c0 += 32) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, r);
+                ptx::tmem_ld_wait();
+                if (c0 + 32 >= ncol) {  // accumulator fully read: the next item may start
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(acc_empty);
+                }
+                if (!jvalid) continue;
+                const int nvalid = min(32, ncol - c0);
+                const int fb = gi * g.kpg + f_tile0 + c0;
+                float* dst = p.out + obase + (int64_t)fb * ostride;
+                if (p.add_mode) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (e < nvalid) dst[(int64_t)e * ostride] += __uint_as_float(r[e]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (e < nvalid)
+                            dst[(int64_t)e * ostride] =
+                                __uint_as_float(r[e]) + (p.bias ? __ldg(p.bias + fb + e) : 0.f);
+                }
+            }
+        }
+    } else if (warp == G8_ATMA_WARP) {
+        // ============================ A chunks by TMA (matrix sources) ==================
+        if (p.tma_a) {
+            const uint32_t leader = ptx::elect_one();
+            int64_t cbase = 0;
+            for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch) {
+                int nt, gi;
+                int64_t mt;
+                decode(t, nt, mt, gi);
+                const int x0 = (int)(p.pm.j_begin + mt * G8_BM);
+                const int row0 = gi * g.kdim;
+                const int64_t sl = p.tps ? mt / p.tps : 0;
+                const int xs = p.tps ? (int)(mt - sl * p.tps) * G8_BM : 0;
+                for (int kc = 0; kc < nch; ++kc) {
+                    const int64_t cg = cbase + kc;
+                    const int as = (int)(cg % G8_ASTAGES);
+                    ptx::mbar_wait(&as_empty[as], (uint32_t)(((cg / G8_ASTAGES) & 1) ^ 1));
+                    if (leader) {
+                        ptx::mbar_arrive_expect_tx(&as_full[as], G8_ASTAGE_BYTES);
+                        if (p.tps)  // slice buffer as {np, kdim, slices}
+                            ptx::tma_load_3d(astage + (size_t)as * (32 * G8_BM), &tm_a, &as_full[as], xs,
+                                             kc * G8_CK, (int32_t)sl);
+                        else
+                            ptx::tma_load_2d(astage + (size_t)as * (32 * G8_BM), &tm_a, &as_full[as], x0,
+                                             row0 + kc * G8_CK);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp == G8_TMA_WARP) {
+        // ============================ weight TMA =========================================
+        const uint32_t leader = ptx::elect_one();
+        const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
+        int64_t sbase = 0;
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, sbase += nstage) {
+            int nt, gi;
+            int64_t mt;
+            decode(t, nt, mt, gi);
+            const int row0 = gi * g.kpg + nt * BN;
+            for (int kb = 0; kb < nstage; ++kb) {
+                const int64_t sg = sbase + kb;
+                const int s = (int)(sg % p.bstages);
+                const uint32_t ph = (uint32_t)((sg / p.bstages) & 1);
+                ptx::mbar_wait(&b_empty[s], ph ^ 1);
+                if (leader) {
+                    uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&b_full[s], Cfg::STAGE_BYTES);
+                    ptx::tma_load_2d(st, &tm_hi, &b_full[s], kb * Cfg::KE, row0);
+                    ptx::tma_load_2d(st + Cfg::B_BYTES, &tm_lo, &b_full[s], kb * Cfg::KE, row0);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ============================ MMA issuer ========================================
+        const uint32_t leader = ptx::elect_one();
+        constexpr uint32_t idesc = ptx::idesc_f32acc<BF16>(G8_BM, BN);
+        const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(smem));
+        constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
+        const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
+        int64_t cbase = 0, sbase = 0;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++i, cbase += nch, sbase += nstage) {
+            ptx::mbar_wait(acc_empty, (i & 1) ^ 1);
+            ptx::tc_fence_after();
+            for (int kc = 0; kc < nch; ++kc) {
+                const int64_t cg = cbase + kc;
+                const int slot = (int)(cg % p.ring);
+                const int64_t sg = sbase + kc / Cfg::CPS;
+                const int s = (int)(sg % p.bstages);
+                if (kc % Cfg::CPS == 0) ptx::mbar_wait(&b_full[s], (uint32_t)((sg / p.bstages) & 1));
+                ptx::mbar_wait(&a_full[slot], (uint32_t)((cg / p.ring) & 1));
+                ptx::tc_fence_after();
+                if (leader) {
+                    const uint32_t a_hi = tmem_base + BN + slot * Cfg::CHUNK_COLS;
+                    const uint32_t a_lo = a_hi + Cfg::HALF_COLS;
+                    const uint64_t sb = db0 + (uint64_t)(s * STG16) + (kc % Cfg::CPS) * (G8_CK * Cfg::EB / 16);
+#pragma unroll
+                    for (int u = 0; u < G8_CK / Cfg::UK; ++u) {
+                        const uint64_t dbh = sb + 2 * u, dbl = dbh + BLO16;
+                        const uint32_t first = (kc > 0 || u > 0) ? 1u : 0u;
+                        ptx::umma_ts<BF16>(tmem_base, a_lo + u * 8, dbh, idesc, first);
+                        ptx::umma_ts<BF16>(tmem_base, a_hi + u * 8, dbl, idesc, 1u);
+                        ptx::umma_ts<BF16>(tmem_base, a_hi + u * 8, dbh, idesc, 1u);
+                    }
+                    ptx::umma_commit(&a_empty[slot]);
+                    if (kc % Cfg::CPS == Cfg::CPS - 1 || kc == nch - 1) ptx::umma_commit(&b_empty[s]);
+                }
+                __syncwarp();
+            }
+            if (leader) ptx::umma_commit(acc_full);
+            __syncwarp();
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == G8_MMA_WARP) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, G8_TMEM_COLS);
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// Host side
+// ----------------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g8_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+template <int BN, bool BF16>
+static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w_lo, cudaStream_t st) {
+    using Cfg = G8Cfg<BN, BF16>;
+    G8Params prm = prm_in;
+    prm.ring = (G8_TMEM_COLS - BN) / Cfg::CHUNK_COLS;
+    prm.bstages = std::min(8, (200 * 1024 - G8_ASTAGES * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
+    const size_t smem = 1024 + (size_t)prm.bstages * Cfg::STAGE_BYTES + G8_ASTAGES * G8_ASTAGE_BYTES +
+                        8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * G8_ASTAGES);
+    auto kern = gemm_ts_kernel<BN, BF16>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    if (attr_err != cudaSuccess)
+        return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    auto enc = g8_encode_fn();
+    if (!enc) return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if ((reinterpret_cast<uintptr_t>(w_hi) | reinterpret_cast<uintptr_t>(w_lo)) & 15)
+        return fail(CB_ERR_MISALIGNED, "split weights must be 16-byte aligned");
+    CUtensorMap mh, ml;
+    for (int h = 0; h < 2; ++h) {
+        cuuint64_t dims[2] = {(cuuint64_t)prm.g.kdim_pad, (cuuint64_t)prm.g.K};
+        cuuint64_t strides[1] = {(cuuint64_t)prm.g.kdim_pad * Cfg::EB};
+        cuuint32_t box[2] = {(cuuint32_t)Cfg::KE, (cuuint32_t)BN};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(h ? &ml : &mh, BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         2, const_cast<void*>(h ? w_lo : w_hi), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string((int)r));
+    }
+    CUtensorMap ma{};
+    if (prm.tma_a && prm.tps) {  // slices [count][kdim][np], boxes of 128 pixels x 32 rows
+        cuuint64_t dims[3] = {(cuuint64_t)prm.np, (cuuint64_t)prm.g.kdim,
+                              (cuuint64_t)(prm.pm.j_count / prm.np)};
+        cuuint64_t strides[2] = {(cuuint64_t)prm.np * 4, (cuuint64_t)prm.g.kdim * prm.np * 4};
+        cuuint32_t box[3] = {(cuuint32_t)G8_BM, (cuuint32_t)G8_CK, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(prm.src), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (slices) failed: " + std::to_string((int)r));
+    } else if (prm.tma_a) {  // the fp32 matrix [rows][ld], boxes of 128 pixels x 32 rows
+        cuuint64_t dims[2] = {(cuuint64_t)prm.pm.src_ld, (cuuint64_t)prm.g.G * prm.g.kdim};
+        cuuint64_t strides[1] = {(cuuint64_t)prm.pm.src_ld * 4};
+        cuuint32_t box[2] = {(cuuint32_t)G8_BM, (cuuint32_t)G8_CK};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(prm.src), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)r));
+    }
+    const int grid = (int)std::min<int64_t>(prm.items, sm_count());
+    kern<<<grid, G8_THREADS, std::max<size_t>(smem, 120 * 1024), st>>>(prm, mh, ml, ma);
+    return check_launch("gemm_ts_kernel");
+}
+
+// Matrix / slice sources only (the stepwise GEMMs).  Returns CB_ERR_UNSUPPORTED when the
+// caller should fall back to K4.
+int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
+                   const void* w_lo, const float* bias, float* out, int add_mode, cudaStream_t st) {
+    if (pm.src_mode == SRC_CONV || std::getenv("CB_NO_K8")) return CB_ERR_UNSUPPORTED;
+    if (pm.j_count == 0) return CB_OK;
+    G8Params prm{};
+    prm.g = g;
+    prm.pm = pm;
+    prm.src = src;
+    prm.bias = add_mode ? nullptr : bias;
+    prm.out = out;
+    prm.add_mode = add_mode;
+    prm.nchunks = (g.kdim + G8_CK - 1) / G8_CK;
+    const int bn = g.kpg <= 64 ? 64 : g.kpg <= 128 ? 128 : 256;
+    prm.m_tiles = (pm.j_count + G8_BM - 1) / G8_BM;
+    const bool slice_tma = pm.src_mode == SRC_SLICES && pm.band_rows > 0 &&
+                           g.P % pm.band_rows == 0 && (pm.band_rows * g.Q) % 4 == 0 &&
+                           pm.j_count % (pm.band_rows * g.Q) == 0 &&
+                           (reinterpret_cast<uintptr_t>(src) & 15) == 0 && !std::getenv("CB_K8_NO_TMA_A");
+    if (slice_tma) {  // slice-aligned tiles
+        const int npx = pm.band_rows * g.Q;
+        prm.m_tiles = (pm.j_count / npx) * ((npx + G8_BM - 1) / G8_BM);
+    }
+    // (narrower channel tiles for short grids measured slower: A is rebuilt per channel tile)
+    prm.n_tiles = (g.kpg + bn - 1) / bn;
+    prm.items = prm.m_tiles * prm.n_tiles * g.G;
+    prm.tma_a = pm.src_mode == SRC_MATRIX && (pm.src_ld % 4) == 0 &&
+                (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pm.j_begin + pm.j_count <= pm.src_ld &&
+                !std::getenv("CB_K8_NO_TMA_A");
+    // SConv slices: equal slices (P a multiple of the band) of a 16-byte multiple of pixels
+    // -> slice-aligned tiles, A chunks by a 3-D TMA over {np, kdim, slices}
+    const int np = pm.band_rows * g.Q;
+    if (slice_tma) {
+        prm.tma_a = 1;
+        prm.np = np;
+        prm.tps = (np + G8_BM - 1) / G8_BM;
+    }
+    switch (bn) {
+        case 64: return bf16 ? launch_g8_cfg<64, true>(prm, w_hi, w_lo, st) : launch_g8_cfg<64, false>(prm, w_hi, w_lo, st);
+        case 128: return bf16 ? launch_g8_cfg<128, true>(prm, w_hi, w_lo, st) : launch_g8_cfg<128, false>(prm, w_hi, w_lo, st);
+        default: return bf16 ? launch_g8_cfg<256, true>(prm, w_hi, w_lo, st) : launch_g8_cfg<256, false>(prm, w_hi, w_lo, st);
+    }
+}
+
+}  // namespace cb
