@@ -396,12 +396,63 @@ int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float
     return check_launch("weight_split");
 }
 
+// K5 by rows: a slice is a band of whole output rows of one image, so each (slice, channel)
+// pair is one contiguous run in both the accumulator buffer and y.  One warp per run, float4
+// when both ends are 16-byte aligned.
+__global__ void __launch_bounds__(256)
+unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int64_t nrows,
+                   const float* __restrict__ acc, const float* __restrict__ bias,
+                   float* __restrict__ y) {
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= nrows) return;
+    const int64_t ls = row / g.K;
+    const int f = (int)(row - ls * g.K);
+    const int per_img = (g.P + band_rows - 1) / band_rows;
+    const int64_t sg = s_first + ls;
+    const int64_t n = sg / per_img;
+    const int y0 = (int)(sg - n * per_img) * band_rows;
+    const int np = min(band_rows, g.P - y0) * g.Q;
+    const int64_t j0 = n * g.PQ + (int64_t)y0 * g.Q;
+    const float* src = acc + (int64_t)g.K * (j0 - j_begin) + (int64_t)f * np;
+    float* dst = y + (n * g.K + f) * g.PQ + (int64_t)y0 * g.Q;
+    const float b = bias ? __ldg(bias + f) : 0.f;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const int n4 = np >> 2;
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (int i = lane; i < n4; i += 32) {
+            float4 v = __ldg(s4 + i);
+            v.x += b; v.y += b; v.z += b; v.w += b;
+            d4[i] = v;
+        }
+        for (int i = (n4 << 2) + lane; i < np; i += 32) dst[i] = __ldg(src + i) + b;
+    } else {
+        for (int i = lane; i < np; i += 32) dst[i] = __ldg(src + i) + b;
+    }
+}
+
 int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count,
                   const float* acc, const float* bias, float* y, cudaStream_t st) {
     const int64_t total = j_count * g.K;
     if (total == 0) return CB_OK;
-    unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>(g, band_rows, j_begin, j_count, acc,
-                                                         bias, y);
+    // the launch covers whole slices: count them from the first slice's index
+    const int per_img = (g.P + band_rows - 1) / band_rows;
+    const int64_t n0 = j_begin / g.PQ;
+    const int oy0 = (int)((j_begin - n0 * g.PQ) / g.Q);
+    const int64_t s_first = n0 * per_img + oy0 / band_rows;
+    int64_t nslices = 0;
+    for (int64_t j = j_begin; j < j_begin + j_count; ++nslices) {
+        const int64_t sg = s_first + nslices;
+        const int64_t n = sg / per_img;
+        const int y0 = (int)(sg - n * per_img) * band_rows;
+        j = n * g.PQ + (int64_t)y0 * g.Q + (int64_t)std::min(band_rows, g.P - y0) * g.Q;
+    }
+    const int64_t nrows = nslices * g.K;
+    const int64_t blocks = (nrows + 7) / 8;
+    if (blocks > 0x7fffffffLL) return fail(CB_ERR_UNSUPPORTED, "unpack grid too large");
+    unpack_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, band_rows, s_first, j_begin, nrows,
+                                                          acc, bias, y);
     return check_launch("unpack");
 }
 
