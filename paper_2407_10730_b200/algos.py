@@ -49,6 +49,7 @@ from .timing import HOST_PHASES, Phase, PhaseLedger
 DEFAULT_VARIANT = "tc3xtf32"
 FUSED_DEFAULT_VARIANT = "tc3xbf16"
 B200_L2_BYTES = 126 * 1024 * 1024
+SCONV_CHUNK_MIN_BYTES = 1 << 30
 _DESC_FIELDS = tuple(f.name for f in fields(ConvDescriptor))
 
 __all__ = [
@@ -401,16 +402,20 @@ def _plan_sconv_cached(desc: ConvDescriptor, cache: CacheParams) -> SConvPlan:
 
 def plan_sconv(desc, cache: CacheParams | None = None) -> SConvPlan:
     """GPU slice plan (the role of _plan_tiles, algos.py:254-262): slices are bands of
-    output rows; consecutive slices are grouped into chunks whose packed slices plus
-    accumulators fit in half the L2, so pack -> microkernel -> unpack of a chunk stays
-    on chip."""
+    output rows; consecutive slices are grouped into chunks of at most
+    max(half the L2, 1 GiB) of packed slices plus accumulators (an explicit `cache` bounds
+    chunks by its L2 alone)."""
+    explicit = cache is not None
     cache = cache if cache is not None else CacheParams()
     lib = _capi.load()
     d = desc
     oh, ow = output_shape(d)
     kdim = d.in_channels * d.k_h * d.k_w
     per_pixel = 4 * (kdim + d.out_channels)
-    budget = max(per_pixel * ow, cache.l2_bytes // 2)
+    # Chunks are sized for the GPU grid, not for L2 residency: measured on cfg4, four
+    # L2-sized chunks (4 x 58 MB) took 532 us and one chunk 283 us -- each extra call leaves
+    # most SMs idle.  The 1 GiB floor still bounds the slice workspace of huge sweep ops.
+    budget = max(per_pixel * ow, cache.l2_bytes // 2, 0 if explicit else SCONV_CHUNK_MIN_BYTES)
     max_slice_px = max(ow, min(oh * ow, budget // per_pixel))
     cd = _cd(d)
     sp = _capi.CbSlicePlan()
@@ -443,7 +448,6 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
     torch = _torch()
     lib = _capi.load()
     pr = _prep(d, variant)
-    cache = cache if cache is not None else CacheParams()
     x, host = _dev(inputs.input)
     w, _ = _dev(inputs.weights)
     w = w.contiguous()
