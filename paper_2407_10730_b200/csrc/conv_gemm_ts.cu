@@ -153,7 +153,11 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             if (jvalid) src_linear(g, p.pm, p.pm.j_begin + jl, lbase, lstride);
             const int64_t row0 = p.pm.src_mode == SRC_MATRIX ? (int64_t)gi * g.kdim : 0;
             const float* srcp = p.src + lbase + row0 * lstride;
-            for (int kc = kpar; kc < nch; kc += 2) {
+            // chunks go to producer groups by GLOBAL chunk parity (cg & 1): each A stage
+            // (cg % 4) is then always consumed by the same group, so its phase parity can never
+            // alias an older phase (with kc parity, an odd chunk count per item would hand a
+            // stage to the other group on the next item -- an ABA race on the mbarrier phase)
+            for (int kc = (int)((kpar - cbase) & 1); kc < nch; kc += 2) {
                 const int64_t cg = cbase + kc;
                 const int slot = (int)(cg % p.ring);
                 const uint32_t ph = (uint32_t)((cg / p.ring) & 1);
@@ -372,6 +376,7 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
     G8Params prm = prm_in;
     prm.ring = (G8_TMEM_COLS - BN) / Cfg::CHUNK_COLS;
     prm.bstages = std::min(8, (200 * 1024 - G8_ASTAGES * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
+    if (const char* e = std::getenv("CB_K8_BSTAGES")) prm.bstages = std::max(2, std::min(prm.bstages, std::atoi(e)));
     const size_t smem = 1024 + (size_t)prm.bstages * Cfg::STAGE_BYTES + G8_ASTAGES * G8_ASTAGE_BYTES +
                         8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * G8_ASTAGES);
     auto kern = gemm_ts_kernel<BN, BF16>;

@@ -264,3 +264,22 @@ def test_stacked_taps_match_oracle(cuda, variant, spec):
     assert fused_layout(d, variant)["path"] == 1  # TMA kernel on the stacked 1x1 geometry
     inp, (x, w, b) = _inputs(d)
     _check_conv(d, conv_fused(inp, variant=variant), orc.conv_direct_naive(d, x, w, b))
+
+
+@pytest.mark.parametrize("variant", ["tc3xtf32", "tc3xbf16"])
+def test_stepwise_gemm_odd_chunk_counts(cuda, variant):
+    """K8 with an odd number of 32-wide reduction chunks per item and several items per CTA
+    (the chunk-to-producer-group assignment must stay fixed across items), back to back."""
+    from paper_2407_10730_b200.algos import conv_baseline_im2col_gemm, conv_main_blocked_direct
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    from paper_2407_10730_b200.timing import PhaseLedger
+    shapes = [ConvDescriptor(batch=1, in_channels=32, in_h=28, in_w=28, out_channels=32, k_h=1,
+                             k_w=1, stride_h=2, stride_w=2),                       # 1 chunk
+              ConvDescriptor(batch=1, in_channels=32, in_h=164, in_w=164, out_channels=32, k_h=3,
+                             k_w=3, pad_h=1, pad_w=1)]                             # 9 chunks, 211 tiles
+    for _ in range(2):
+        for d in shapes:
+            inp, (x, w, b) = _inputs(d)
+            ref = orc.conv_direct_naive(d, x, w, b)
+            for fn in (conv_baseline_im2col_gemm, conv_main_blocked_direct):
+                _check_conv(d, fn(inp, PhaseLedger(), variant=variant), ref)

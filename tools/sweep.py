@@ -84,6 +84,9 @@ def main(argv=None) -> int:
                     help="time each op as a replayed CUDA graph (kernels without host launch gaps)")
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip larger ops (0: none)")
     ap.add_argument("--out", default="sweep_out")
+    ap.add_argument("--verbose", action="store_true", help="print every op key before it runs")
+    ap.add_argument("--skip", type=int, default=0, help="diagnostics: skip this rank's first N ops")
+    ap.add_argument("--limit", type=int, default=0, help="diagnostics: run at most N ops (0: all)")
     args = ap.parse_args(argv)
 
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -102,6 +105,7 @@ def main(argv=None) -> int:
     peaks = roofline.load_peaks()
     cost = [predicted_s(descs[i], peaks) for i in idx]
     mine = [idx[j] for j in lpt_assign(cost, world)[rank]]
+    mine = mine[args.skip:args.skip + args.limit] if args.limit else mine[args.skip:]
     modes = [m for m in args.modes.split(",") if m]
     inputs_fn = harness.device_inputs if args.device_inputs else None
 
@@ -113,6 +117,8 @@ def main(argv=None) -> int:
         cfg = harness.RunConfig(mode=m, warmups=args.warmups, runs=args.runs,
                                 seed=args.data_seed, variant=variant, graph=args.graph)
         for n, i in enumerate(mine):
+            if args.verbose:
+                print(f"[{m} {n}] {i} {descs[i]}", flush=True)
             o = harness.run_single(descs[i], cfg, inputs_fn=inputs_fn)
             rf = roofline.conv_roofline(descs[i], variant, peaks)
             t_op = o.stats.operation_ns_mean * 1e-9 if o.stats else None
