@@ -223,7 +223,8 @@ def run_ours(args):
     from paper_2407_10730_b200.timing import EventLedger, Phase
 
     rank, world, local = dist_env()
-    variant = args.variant or algos.FUSED_DEFAULT_VARIANT
+    variant = algos.resolve_variant(workload(args.config, world, args.scaling, rank),
+                                    args.variant or algos.FUSED_AUTO)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

@@ -48,6 +48,18 @@ from .timing import HOST_PHASES, Phase, PhaseLedger
 # lower, K-independent error.
 DEFAULT_VARIANT = "tc3xtf32"
 FUSED_DEFAULT_VARIANT = "tc3xbf16"
+# "auto" (the fused entry points' default): the FFMA kernel for small convolutions -- one
+# launch on raw NCHW / OIHW, no split passes -- else 3xBF16.  On the config-5 sample, FFMA
+# ops were faster below ~1e8 FLOPs (median 21 vs 36 us) and far slower above ~1e9.
+FUSED_AUTO = "auto"
+AUTO_FFMA_MAX_FLOPS = 1.5e8
+
+
+def resolve_variant(desc, variant: str) -> str:
+    """The concrete variant `variant` names for this descriptor ("auto" -> ffma or tc3xbf16)."""
+    if variant != FUSED_AUTO:
+        return variant
+    return "ffma" if flop_count(desc) < AUTO_FFMA_MAX_FLOPS else FUSED_DEFAULT_VARIANT
 B200_L2_BYTES = 126 * 1024 * 1024
 SCONV_CHUNK_MIN_BYTES = 1 << 30
 _DESC_FIELDS = tuple(f.name for f in fields(ConvDescriptor))
@@ -56,7 +68,7 @@ __all__ = [
     "CacheParams", "ConvInputs", "GemmBlocking", "UnsupportedDescriptorError",
     "conv_baseline_im2col_gemm", "conv_fused", "conv_main_blocked_direct", "gemm",
     "im2col_transform", "split_weights", "plan_tiles", "plan_sconv", "DEFAULT_VARIANT",
-    "FUSED_DEFAULT_VARIANT", "fused_layout", "fused_plan", "pack_fused_weights", "fused_workspace",
+    "FUSED_DEFAULT_VARIANT", "FUSED_AUTO", "resolve_variant", "fused_layout", "fused_plan", "pack_fused_weights", "fused_workspace",
 ]
 
 
@@ -499,6 +511,7 @@ def _fused_layout_cached(desc, variant: str, env: tuple) -> tuple:
 
 
 def fused_layout(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
+    variant = resolve_variant(desc, variant)
     """cb_fused_layout_query: path (1 = TMA im2col, 0 = gather), chunking, workspace.
     Cached per (descriptor, variant): it is pure host arithmetic."""
     return dict(_fused_layout_cached(ConvDescriptor(**{f: getattr(desc, f) for f in _DESC_FIELDS}),
@@ -506,6 +519,7 @@ def fused_layout(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
 
 
 def fused_plan(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
+    variant = resolve_variant(desc, variant)
     tp = _capi.CbTilePlan()
     _capi.check(_capi.load().cb_fused_plan_tiles(_capi.variant_id(variant),
                                                  ctypes.byref(_cd(desc)), ctypes.byref(tp)))
@@ -513,6 +527,7 @@ def fused_plan(desc, variant: str = FUSED_DEFAULT_VARIANT) -> dict:
 
 
 def pack_fused_weights(w_dev, desc, variant: str = FUSED_DEFAULT_VARIANT):
+    variant = resolve_variant(desc, variant)
     """(w_hi, w_lo, w_f32) in the layout conv_fused's kernel consumes (K3, fused layout)."""
     torch = _torch()
     if variant not in _capi.TC_VARIANTS:
@@ -528,13 +543,14 @@ def pack_fused_weights(w_dev, desc, variant: str = FUSED_DEFAULT_VARIANT):
 
 
 def fused_workspace(desc, variant: str = FUSED_DEFAULT_VARIANT, device="cuda"):
+    variant = resolve_variant(desc, variant)
     n = fused_layout(desc, variant)["workspace_bytes"]
     if n == 0:
         return None
     return _torch().empty(n, dtype=_torch().uint8, device=device)
 
 
-def conv_fused(inputs, ledger=None, *, variant: str = FUSED_DEFAULT_VARIANT, packed=None,
+def conv_fused(inputs, ledger=None, *, variant: str = FUSED_AUTO, packed=None,
                workspace=None, out=None):
     """y = conv(x, w) + b as the fused implicit-GEMM convolution.
 
@@ -546,6 +562,7 @@ def conv_fused(inputs, ledger=None, *, variant: str = FUSED_DEFAULT_VARIANT, pac
     torch = _torch()
     lib = _capi.load()
     d = inputs.desc
+    variant = resolve_variant(d, variant)
     pr = _prep(d, variant)
     x, host = _dev(inputs.input)
     b = _dev(inputs.bias)[0] if inputs.bias is not None else None
@@ -595,9 +612,10 @@ class FusedConv:
     several ctypes calls (the GPU-native replacement for a tracing compiler).  A FusedConv
     owns one workspace: do not run the same object concurrently on two streams."""
 
-    def __init__(self, desc, variant: str = FUSED_DEFAULT_VARIANT, device="cuda"):
+    def __init__(self, desc, variant: str = FUSED_AUTO, device="cuda"):
         torch = _torch()
         self.desc = desc
+        variant = resolve_variant(desc, variant)
         self.variant = variant
         self.vid = _capi.variant_id(variant)
         self._cd = _cd(desc)
@@ -687,7 +705,7 @@ class HostPipeline:
     the transfers in flight concurrently instead of back to back.  Pinned host buffers make
     the copies asynchronous.  synchronize() waits for every submitted step."""
 
-    def __init__(self, desc, variant: str = FUSED_DEFAULT_VARIANT, depth: int = 2,
+    def __init__(self, desc, variant: str = FUSED_AUTO, depth: int = 2,
                  device="cuda"):
         torch = _torch()
         self.desc = desc

@@ -78,7 +78,7 @@ def main(argv=None) -> int:
     ap.add_argument("--warmups", type=int, default=3)
     ap.add_argument("--runs", type=int, default=10)
     ap.add_argument("--variant", default=None, help="stepwise variant (default tc3xtf32)")
-    ap.add_argument("--fused-variant", default=algos.FUSED_DEFAULT_VARIANT)
+    ap.add_argument("--fused-variant", default=algos.FUSED_AUTO)
     ap.add_argument("--device-inputs", action="store_true")
     ap.add_argument("--graph", action="store_true",
                     help="time each op as a replayed CUDA graph (kernels without host launch gaps)")
@@ -120,7 +120,7 @@ def main(argv=None) -> int:
             if args.verbose:
                 print(f"[{m} {n}] {i} {descs[i]}", flush=True)
             o = harness.run_single(descs[i], cfg, inputs_fn=inputs_fn)
-            rf = roofline.conv_roofline(descs[i], variant, peaks)
+            rf = roofline.conv_roofline(descs[i], algos.resolve_variant(descs[i], variant), peaks)
             t_op = o.stats.operation_ns_mean * 1e-9 if o.stats else None
             if t_op:
                 busy[m] += t_op
