@@ -64,3 +64,16 @@ def test_stratified_sample_and_lpt_cover_the_sweep():
     assert sorted(j for p in parts for j in p) == list(range(len(a)))
     loads = [sum(cost[j] for j in p) for p in parts]
     assert max(loads) <= sum(loads) / 4 + max(cost) + 1e-12
+
+
+def test_model_op_set_is_valid():
+    """configs/model_ops.json (tools/model_ops.py): every layer key parses into a valid
+    descriptor, and the unique list covers exactly the layers of all models."""
+    import json
+    from paper_2407_10730_b200.descriptor import key_of, parse_key
+    data = json.loads((ROOT / "configs" / "model_ops.json").read_text())
+    layers = [k for m in data["models"].values() for k in m["layers"]]
+    assert set(layers) == set(data["unique"]) and len(data["unique"]) >= 300
+    for k in data["unique"]:
+        assert key_of(parse_key(k)) == k
+    assert data["models"]["resnet50"]["layers"][0].startswith("n1_c3x224x224_f64x7x7_s2x2_p3x3")

@@ -70,6 +70,9 @@ def pct(vals, q):
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--opset", choices=["synthetic", "models"], default="synthetic",
+                    help="synthetic: BASELINE config 5; models: configs/model_ops.json "
+                         "(torchvision layers, tools/model_ops.py)")
     ap.add_argument("--ops", type=int, default=configs.SWEEP_SIZE)
     ap.add_argument("--seed", type=int, default=0, help="sweep generator seed")
     ap.add_argument("--data-seed", type=int, default=0, help="make_inputs seed")
@@ -98,7 +101,14 @@ def main(argv=None) -> int:
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
 
-    descs = configs.sweep(args.ops, args.seed)
+    model_ops = None
+    if args.opset == "models":
+        from paper_2407_10730_b200.descriptor import parse_key
+        model_ops = json.loads((Path(__file__).resolve().parent.parent / "configs" /
+                                "model_ops.json").read_text())
+        descs = [parse_key(k) for k in model_ops["unique"]]
+    else:
+        descs = configs.sweep(args.ops, args.seed)
     idx = stratified_sample(descs, args.sample, args.seed) if args.sample else list(range(len(descs)))
     if args.max_gflop > 0:
         idx = [i for i in idx if flop_count(descs[i]) <= args.max_gflop * 1e9]
@@ -175,6 +185,17 @@ def main(argv=None) -> int:
                 "per_rank_busy_s": [g["busy"][m] for g in gathered],
                 "failed": [(r["index"], r["detail"]) for r in rows if r["status"] == "failed"][:20],
             }
+        if model_ops is not None:  # per-model conv time: every layer, in network order
+            from paper_2407_10730_b200.descriptor import key_of
+            t_of = {m: {key_of(descs[r["index"]]): r["t_s"] for g in gathered for r in g["rows"][m]}
+                    for m in modes}
+            summary["opset"] = model_ops["source"]
+            summary["models"] = {
+                name: {"layers": len(mo["layers"]),
+                       **{f"{m}_conv_ms": (sum(t_of[m].get(k) or 0.0 for k in mo["layers"]) * 1e3
+                                           if all(t_of[m].get(k) for k in mo["layers"]) else None)
+                          for m in modes}}
+                for name, mo in model_ops["models"].items()}
         (out / "summary.json").write_text(json.dumps(summary, indent=1) + "\n")
         print(json.dumps({m: {k: v for k, v in s.items() if k != "failed"}
                           for m, s in summary["modes"].items()}, indent=1))
