@@ -285,3 +285,29 @@ def test_stepwise_gemm_odd_chunk_counts(cuda, variant):
             ref = orc.conv_direct_naive(d, x, w, b)
             for fn in (conv_baseline_im2col_gemm, conv_main_blocked_direct):
                 _check_conv(d, fn(inp, PhaseLedger(), variant=variant), ref)
+
+
+def _model_ops(max_flops: float, step: int):
+    import json
+    from pathlib import Path
+    from paper_2407_10730_b200.descriptor import flop_count, parse_key
+    data = json.loads((Path(__file__).resolve().parent.parent / "configs" / "model_ops.json").read_text())
+    ds = [parse_key(k) for k in data["unique"]]
+    return [d for d in ds if flop_count(d) <= max_flops][::step]
+
+
+@pytest.mark.parametrize("variant", ["tc3xbf16", "auto"])
+def test_model_layers_match_oracle(cuda, variant):
+    """Real-network layers (torchvision, configs/model_ops.json) that are cheap to check:
+    depthwise / grouped / dilated / 1x1 / strided shapes through the fused path and
+    Im2col-GEMM."""
+    from paper_2407_10730_b200.algos import conv_baseline_im2col_gemm, conv_fused
+    from paper_2407_10730_b200.timing import PhaseLedger
+    ops = _model_ops(2e7, 4)
+    assert len(ops) >= 20
+    for d in ops:
+        inp, (x, w, b) = _inputs(d)
+        ref = orc.conv_direct_naive(d, x, w, b)
+        _check_conv(d, conv_fused(inp, variant=variant), ref)
+        if variant == "auto":
+            _check_conv(d, conv_baseline_im2col_gemm(inp, PhaseLedger()), ref)
