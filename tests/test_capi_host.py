@@ -143,3 +143,27 @@ def test_no_cpu_fallback():
                            weights=np.zeros((1, 1, 3, 3), np.float32))
     with pytest.raises(_capi.ConvB200Error, match="no CPU fallback"):
         algos.conv_fused(inp)
+
+
+def test_fused_layout_paths(lib):
+    """Host-side layout choices of the fused conv (cb_fused_layout_query, no GPU needed):
+    K7 for few channels, tap stacking for few output channels, the folded layout, and the
+    'auto' variant rule."""
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.configs import CONFIGS
+    k7 = algos.fused_layout(CONFIGS["cfg3"], "tc3xbf16")  # C=3 stem: direct TMEM kernel
+    assert k7["path"] == 2 and k7["workspace_bytes"] == 0 and k7["weight_cols"] == 192
+    full = ConvDescriptor(batch=1, in_channels=128, in_h=12, in_w=12, out_channels=8, k_h=3,
+                          k_w=3, pad_h=1, pad_w=1)  # R*S*K = 72 <= 256: all taps stacked
+    lay = algos.fused_layout(full, "tc3xbf16")
+    assert lay["path"] == 1 and lay["weight_rows"] == 9 * 8 and lay["weight_cols"] == 128
+    assert lay["workspace_bytes"] >= 9 * 8 * 12 * 12 * 4  # + the stacked planes Y'
+    row = ConvDescriptor(batch=1, in_channels=64, in_h=19, in_w=21, out_channels=32, k_h=7,
+                         k_w=7, pad_h=3, pad_w=3)  # S*K = 224: the 7 horizontal taps stacked
+    assert algos.fused_layout(row, "tc3xbf16")["weight_rows"] == 7 * 32
+    fold = ConvDescriptor(batch=1, in_channels=24, in_h=20, in_w=20, out_channels=64, k_h=5,
+                          k_w=5, pad_h=2, pad_w=2)  # 25 taps of 32 -> 5 folded rows of 120
+    assert algos.fused_layout(fold, "tc3xbf16")["k_blocks"] == 10
+    assert algos.resolve_variant(CONFIGS["cfg1"], "auto") == "tc3xbf16"
+    assert algos.resolve_variant(CONFIGS["cfg2a"], "auto") == "ffma"
+    assert algos.resolve_variant(CONFIGS["cfg4"], "tc3xtf32") == "tc3xtf32"
