@@ -44,16 +44,25 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", str(ROOT / "include"), "-I", str(CSRC), "--expt-relaxed-constexpr",
               "-Xptxas", "-v" if verbose else "-O3"]
-    objs = []
-    for src in SOURCES:
+    shared = [CSRC / h for h in HEADERS] + [ROOT / "include" / "convb200.h", Path(__file__)]
+    newest_shared = max(p.stat().st_mtime for p in shared)
+
+    def compile_one(src: str) -> str:
         obj = objdir / (Path(src).stem + ".o")
+        if (not force and obj.exists() and obj.stat().st_mtime > newest_shared
+                and obj.stat().st_mtime > (CSRC / src).stat().st_mtime):
+            return str(obj)  # object is newer than its source and every shared header
         cmd = [*common, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
         if verbose and r.stderr:
             print(r.stderr, file=sys.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs, "-lcuda"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -917,7 +917,7 @@ int launch_fill_bias(int64_t images, int K, int PQ, const float* bias, float* y,
 // globaltimer values of the latest launch, read back with cb_debug_trace().
 static unsigned long long* g_trace = nullptr;
 static int g_trace_ctas = 0;
-static unsigned long long* debug_trace_buffer(int ctas, cudaStream_t st) {
+unsigned long long* debug_trace_buffer(int ctas, cudaStream_t st) {
     const size_t n = (size_t)1024 * TRACE_SLOTS;
     if (!g_trace && cudaMalloc(&g_trace, n * sizeof(unsigned long long)) != cudaSuccess)
         g_trace = nullptr;

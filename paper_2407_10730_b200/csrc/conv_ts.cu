@@ -52,12 +52,53 @@ struct TsParams {
     uint32_t w_half_bytes;  // n_pad * kb_w * 2
     int debug;              // diagnostics (CB_TS_DEBUG): 1 no MMA, 2 no tcgen05.st, 4 no input TMA
     int tma_store;          // 1: epilogue stages 32-channel chunks in smem, TMA stores them
+    float inv_q;            // 1 / Q (pixel -> output row without an integer division)
+    int fixed;              // CB_TS_FIXED_LIST id of a compile-time producer, 0: generic
+    unsigned long long* trace;  // diagnostics (CB_TS_TRACE): clock64 stamps of CTAs 0..3
 };
+
+// Persistent tile walk without 64-bit divisions: tile t = n * tiles_per_img + ti, advanced
+// by gridDim.x = step_n * tiles_per_img + step_ti.
+struct TileWalk {
+    int t, n, ti, step_n, step_ti;
+    __device__ __forceinline__ explicit TileWalk(const struct TsParams& p);
+    __device__ __forceinline__ void next(const struct TsParams& p);
+};
+
+// trace layout: [cta < 4][event < 16][local tile < 512]
+__device__ __forceinline__ void ts_stamp(const TsParams& p, int e, int i) {
+    if (p.trace && blockIdx.x < 4 && i < 512) p.trace[blockIdx.x * 8192 + e * 512 + i] = clock64();
+}
+
+__device__ __forceinline__ TileWalk::TileWalk(const TsParams& p) {
+    t = blockIdx.x;
+    n = t / p.tiles_per_img;
+    ti = t - n * p.tiles_per_img;
+    step_n = gridDim.x / p.tiles_per_img;
+    step_ti = gridDim.x - step_n * p.tiles_per_img;
+}
+__device__ __forceinline__ void TileWalk::next(const TsParams& p) {
+    t += gridDim.x;
+    n += step_n;
+    ti += step_ti;
+    if (ti >= p.tiles_per_img) {
+        ti -= p.tiles_per_img;
+        ++n;
+    }
+}
+// v / Q for 0 <= v < 2^21: (v + 0.5) / Q stays >= 0.5 / Q away from an integer, far above
+// the float rounding error
+__device__ __forceinline__ int div_q(int v, const TsParams& p) {
+    return __float2int_rz(((float)v + 0.5f) * p.inv_q);
+}
 
 __device__ __forceinline__ float lds_f32(uint32_t a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
     return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
 __device__ __forceinline__ int4 lds_v4(uint32_t a) {
     int4 v;
@@ -73,6 +114,88 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo_elem, float hi_elem) {
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
     return d;
 }
+
+// (hi, lo) bf16 pair words of two fp32 values: hi = (bf16(v0), bf16(v1)), lo = the rounded
+// residuals, element v0 in bits 0..15
+__device__ __forceinline__ void split_pair(float v0, float v1, uint32_t& hi, uint32_t& lo) {
+    hi = bf16x2_rn(v0, v1);
+    lo = bf16x2_rn(v0 - __uint_as_float(hi << 16), v1 - __uint_as_float(hi & 0xffff0000u));
+}
+
+// A producer with the reduction layout fixed at compile time (C, R, S, unit horizontal
+// dilation): groups [G0, G1) of 8 reduction elements k = (c, r, s), each element one LDS at
+// xs + c * cstride + r * rstride + 4 s (the (c, r) row offsets are loop-invariant, the tap an
+// immediate) -- no offset table, no per-element address arithmetic.  Elements past C*R*S
+// are written as zeros.
+template <int C, int R, int S>
+__device__ __forceinline__ void load_pair(int k, uint32_t xs, uint32_t xa, uint32_t xb, uint32_t cstride,
+                                          uint32_t rstride, bool swap, float& v0, float& v1) {
+    constexpr int KD = C * R * S;
+    const int c = k / (R * S), rs = k % (R * S);
+    if (k + 1 < KD && rs % S + 1 < S) {  // taps (s, s + 1) of one (c, r) row
+        const uint32_t off = c * cstride + (rs / S) * rstride + 4 * (rs % S);
+        v0 = lds_f32(xa + off);  // lanes 16..31 (swap): the second tap
+        v1 = lds_f32(xb + off);
+        if (swap) {
+            const float t = v0;
+            v0 = v1;
+            v1 = t;
+        }
+    } else {
+        v0 = k < KD ? lds_f32(xs + c * cstride + (rs / S) * rstride + 4 * (rs % S)) : 0.f;
+        const int c1 = (k + 1) / (R * S), rs1 = (k + 1) % (R * S);
+        v1 = k + 1 < KD ? lds_f32(xs + c1 * cstride + (rs1 / S) * rstride + 4 * (rs1 % S)) : 0.f;
+    }
+}
+
+// Groups [G0, G1) of 8 elements, software-pipelined: the loads of group g + D are issued
+// before group g is split and stored (the volatile LDS / tcgen05.st asm statements keep
+// their source order, so without this every group would wait out a full LDS latency).
+template <int C, int R, int S, int G0, int G1>
+__device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint32_t rstride,
+                                            uint32_t a_hi, uint32_t a_lo, bool swap) {
+    constexpr int NG = G1 - G0, D = 3;
+    // swap (even horizontal stride): lanes 16..31 load the second tap of an adjacent pair
+    // first, so the warp's 32 addresses (2 words apart per pixel) cover all 32 banks
+    const uint32_t xa = xs + (swap ? 4u : 0u), xb = xs + (swap ? 0u : 4u);
+    float v[D + 1][8];
+#pragma unroll
+    for (int step = 0; step < NG + D; ++step) {
+        if (step < NG) {
+#pragma unroll
+            for (int e = 0; e < 8; e += 2)
+                load_pair<C, R, S>((G0 + step) * 8 + e, xs, xa, xb, cstride, rstride, swap,
+                                   v[step % (D + 1)][e], v[step % (D + 1)][e + 1]);
+        }
+        if (step >= D) {
+            const int gi = step - D;
+            const float* u = v[gi % (D + 1)];
+            uint32_t hv[4], lv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) split_pair(u[2 * e], u[2 * e + 1], hv[e], lv[e]);
+            ptx::tmem_st_32x32b_x4(a_hi + (G0 + gi) * 4, hv);
+            ptx::tmem_st_32x32b_x4(a_lo + (G0 + gi) * 4, lv);
+        }
+    }
+}
+
+// the three producer warps of a lane quadrant take contiguous thirds of the 8-element groups
+template <int C, int R, int S>
+__device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_t cstride,
+                                                 uint32_t rstride, uint32_t a_hi, uint32_t a_lo,
+                                                 bool swap) {
+    constexpr int G = (C * R * S + 7) / 8;
+    constexpr int G1 = (G + 2) / 3, G2 = G1 + (G - G1 + 1) / 2;
+    if (kpart == 0)
+        build_fixed<C, R, S, 0, G1>(xs, cstride, rstride, a_hi, a_lo, swap);
+    else if (kpart == 1)
+        build_fixed<C, R, S, G1, G2>(xs, cstride, rstride, a_hi, a_lo, swap);
+    else
+        build_fixed<C, R, S, G2, G>(xs, cstride, rstride, a_hi, a_lo, swap);
+}
+
+// compile-time reduction layouts (TsParams::fixed): 0 = generic offset-table producer
+#define CB_TS_FIXED_LIST(X) X(1, 3, 7, 7) X(2, 3, 3, 3) X(3, 3, 5, 5) X(4, 4, 3, 3) X(5, 4, 7, 7)
 
 __global__ void __launch_bounds__(TS_THREADS, 1)
 conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUtensorMap tm_x,
@@ -124,6 +247,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) ts_stamp(p, 15, 0);
 
     if (warp < TS_PROD_WARPS) {
         // ============================ A producers ======================================
@@ -147,24 +271,44 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         const int m = quad * 32 + lane;  // pixel row of the tile == TMEM lane
         const uint32_t lane_addr = tmem_base + ((uint32_t)(quad * 32) << 16);
         const int nchunks = p.kp / 32;
+        const bool swap = (g.sw % 2 == 0) && lane >= 16 && !(p.debug & 32);
         int i = 0;
-        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
-            const int n = (int)(t / p.tiles_per_img);
-            const int p0 = (int)(t - (int64_t)n * p.tiles_per_img) * TS_BM;
-            const int oy_a = p0 / g.Q;
+            const int n = tw.n;
+            const int p0 = tw.ti * TS_BM;
+            const int oy_a = div_q(p0, p);
             const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
-            const int oy = pix / g.Q;
+            const int oy = div_q(pix, p);
             const int ox = pix - oy * g.Q;
             const uint32_t xs = ptx::smem_u32(stage0) + b * p.stage_stride +
                                 4u * (uint32_t)((oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw));
             ptx::mbar_wait(&s_full[b], ph);
+            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 1 : 11, i);
             ptx::mbar_wait(&a_empty[b], ph ^ 1);
             ptx::tc_fence_after();
+            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 2 : 12, i);
             const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
             const uint32_t a_lo = a_hi + half_cols;
-            for (int kc = kpart; kc < nchunks && !(p.debug & 16); kc += KPARTS) {
+            if (p.fixed && !(p.debug & 16)) {
+                if (i < 2) {  // columns past the written groups: zero once per A buffer
+                    const uint32_t z[4] = {0u, 0u, 0u, 0u};
+                    for (int c4 = ((g.kdim + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
+                        ptx::tmem_st_32x32b_x4(a_hi + c4, z);
+                        ptx::tmem_st_32x32b_x4(a_lo + c4, z);
+                    }
+                }
+                const uint32_t cstride = 4u * p.box_rows * p.box_w, rstride = 4u * g.dh * p.box_w;
+                switch (p.fixed) {
+#define CB_TS_CASE(id, c, r, s) \
+    case id: build_fixed_part<c, r, s>(kpart, xs, cstride, rstride, a_hi, a_lo, swap); break;
+                    CB_TS_FIXED_LIST(CB_TS_CASE)
+#undef CB_TS_CASE
+                    default: break;
+                }
+            }
+            for (int kc = kpart; kc < nchunks && !p.fixed && !(p.debug & 16); kc += KPARTS) {
                 const uint32_t ko = ptx::smem_u32(koff + kc * 32);
                 uint32_t hv[16], lv[16];
 #pragma unroll
@@ -185,8 +329,10 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                     ptx::tmem_st_32x32b_x16(a_lo + kc * 16, lv);
                 }
             }
+            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 3 : 13, i);
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
+            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 4 : 14, i);
             ptx::mbar_arrive(&a_full[b]);
             ptx::mbar_arrive(&s_empty[b]);
         }
@@ -199,16 +345,17 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         const int m = quad * 32 + lane;
         const bool issuer = threadIdx.x == TS_EPI_WARP0 * 32;
         int i = 0, chunk = 0;
-        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
-            const int n = (int)(t / p.tiles_per_img);
-            const int p0 = (int)(t - (int64_t)n * p.tiles_per_img) * TS_BM;
+            const int n = tw.n;
+            const int p0 = tw.ti * TS_BM;
             const int pix = p0 + m;
             const bool valid = pix < g.PQ;
             float* dst = p.out + (int64_t)n * g.K * g.PQ + pix;
             ptx::mbar_wait(&acc_full[b], ph);
             ptx::tc_fence_after();
+            if (threadIdx.x == TS_EPI_WARP0 * 32) ts_stamp(p, 7, i);
 #pragma unroll 1
             for (int c0 = 0; c0 < g.K; c0 += 32, ++chunk) {
                 uint32_t r[32];
@@ -218,26 +365,29 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 if (c0 + 32 >= g.K) {  // accumulator fully in registers: release it early
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(&acc_empty[b]);
+                    if (threadIdx.x == TS_EPI_WARP0 * 32) ts_stamp(p, 8, i);
                 }
                 if (p.debug & 8) continue;
                 if (p.tma_store) {
                     float* buf = ostage + (chunk & 1) * (32 * TS_BM);
                     if (issuer) ptx::bulk_wait_read<1>();  // the store 2 chunks ago left buf
                     asm volatile("bar.sync 1, 128;" ::: "memory");
+                    const uint32_t bs = ptx::smem_u32(buf + m);
                     if (p.bias) {
 #pragma unroll
                         for (int e = 0; e < 32; ++e)
-                            buf[e * TS_BM + m] = __uint_as_float(r[e]) +
-                                                 (c0 + e < g.K ? __ldg(p.bias + c0 + e) : 0.f);
+                            sts_f32(bs + 4 * e * TS_BM, __uint_as_float(r[e]) +
+                                                            (c0 + e < g.K ? __ldg(p.bias + c0 + e) : 0.f));
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) buf[e * TS_BM + m] = __uint_as_float(r[e]);
+                        for (int e = 0; e < 32; ++e) sts_f32(bs + 4 * e * TS_BM, __uint_as_float(r[e]));
                     }
                     ptx::fence_proxy_async_smem();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (issuer) {
                         ptx::tma_store_3d(&tm_y, buf, p0, c0, n);
                         ptx::bulk_commit();
+                        ts_stamp(p, 9, i);
                     }
                 } else if (valid) {
 #pragma unroll
@@ -264,13 +414,14 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         }
         __syncwarp();
         int i = 0;
-        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
-            const int n = (int)(t / p.tiles_per_img);
-            const int p0 = (int)(t - (int64_t)n * p.tiles_per_img) * TS_BM;
-            const int iy0 = (p0 / g.Q) * g.sh - g.ph;
+            const int n = tw.n;
+            const int p0 = tw.ti * TS_BM;
+            const int iy0 = div_q(p0, p) * g.sh - g.ph;
             ptx::mbar_wait(&s_empty[b], ph ^ 1);
+            if (leader) ts_stamp(p, 0, i);
             if (leader && (p.debug & 4)) {
                 ptx::mbar_arrive(&s_full[b]);
             } else if (leader) {
@@ -290,12 +441,14 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         const int ksteps = p.kp / 16;
         ptx::mbar_wait(w_full, 0);
         int i = 0;
-        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             ptx::mbar_wait(&a_full[b], ph);
+            if (leader) ts_stamp(p, 5, i);
             ptx::mbar_wait(&acc_empty[b], ph ^ 1);
             ptx::tc_fence_after();
+            if (leader) ts_stamp(p, 6, i);
             const uint32_t d = tmem_base + b * p.n_pad;
             const uint32_t a_hi = tmem_base + col_a0 + b * p.kp;
             const uint32_t a_lo = a_hi + half_cols;
@@ -308,6 +461,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 }
                 ptx::umma_commit(&a_empty[b]);
                 ptx::umma_commit(&acc_full[b]);
+                ts_stamp(p, 10, i);
             }
             __syncwarp();
         }
@@ -332,9 +486,20 @@ struct TsPlan {
     size_t smem;
 };
 
+static int ts_fixed_id(const Geom& g) {
+    if (g.dw != 1 || std::getenv("CB_TS_GENERIC")) return 0;
+#define CB_TS_MATCH(id, c, r, s) \
+    if (g.C == c && g.R == r && g.S == s) return id;
+    CB_TS_FIXED_LIST(CB_TS_MATCH)
+#undef CB_TS_MATCH
+    return 0;
+}
+
 static TsPlan plan_ts(const Geom& g) {
     TsPlan pl{};
     if (g.G != 1 || g.npix == 0) return pl;
+    // int32 tile walk and the float pixel -> row division (TileWalk, div_q)
+    if (g.PQ >= (1 << 21) || (int64_t)g.N * ((g.PQ + TS_BM - 1) / TS_BM) >= (1LL << 31) - 1024) return pl;
     pl.kp = round_up(g.kdim, 32);
     pl.n_pad = round_up(g.K, 16);
     pl.kb_w = round_up(g.kdim, 64);  // == cb_split_kdim(kdim)
@@ -388,6 +553,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode_fn() {
     });
     return fn;
 }
+
+unsigned long long* debug_trace_buffer(int ctas, cudaStream_t st);
 
 int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
                    const float* bias, float* y, cudaStream_t st) {
@@ -446,6 +613,8 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.n_pad = pl.n_pad;
     prm.kb_w = pl.kb_w;
     prm.tiles_per_img = (g.PQ + TS_BM - 1) / TS_BM;
+    prm.inv_q = 1.0f / (float)g.Q;
+    prm.fixed = ts_fixed_id(g);
     prm.total_tiles = (int64_t)g.N * prm.tiles_per_img;
     prm.box_rows = pl.box_rows;
     prm.box_w = pl.box_w;
@@ -454,6 +623,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.stage_stride = pl.stage_stride;
     prm.w_half_bytes = pl.w_half_bytes;
     if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
+    if (std::getenv("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {

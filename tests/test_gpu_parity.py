@@ -311,3 +311,29 @@ def test_model_layers_match_oracle(cuda, variant):
         _check_conv(d, conv_fused(inp, variant=variant), ref)
         if variant == "auto":
             _check_conv(d, conv_baseline_im2col_gemm(inp, PhaseLedger()), ref)
+
+
+# K7 (path 2): every compile-time producer layout (conv_ts.cu CB_TS_FIXED_LIST) and the
+# generic offset-table producer, unit and even horizontal stride (the bank-swap lanes),
+# odd output sizes (a partial last tile), bias, batch > 1, dilation (generic only).
+K7_SHAPES = [(3, 7, 7), (3, 3, 3), (3, 5, 5), (4, 3, 3), (4, 7, 7), (2, 5, 3), (8, 3, 3)]
+
+
+@pytest.mark.parametrize("crs", K7_SHAPES)
+@pytest.mark.parametrize("stride", [1, 2])
+@pytest.mark.parametrize("generic", [False, True])
+def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
+    from paper_2407_10730_b200.algos import conv_fused, fused_layout
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    c, r, s = crs
+    if generic:
+        monkeypatch.setenv("CB_TS_GENERIC", "1")
+    for d in (ConvDescriptor(batch=2, in_channels=c, in_h=37, in_w=44, out_channels=24, k_h=r, k_w=s,
+                             stride_h=stride, stride_w=stride, pad_h=r // 2, pad_w=s // 2, has_bias=True),
+              ConvDescriptor(batch=1, in_channels=c, in_h=20, in_w=28,
+                             out_channels=64 if c * r * s <= 160 else 32, k_h=r, k_w=s,
+                             stride_h=2, stride_w=stride, pad_h=r // 2, pad_w=s // 2, dil_h=2,
+                             dil_w=2 if generic else 1)):
+        assert fused_layout(d, "tc3xbf16")["path"] == 2, d
+        inp, (x, w, b) = _inputs(d)
+        _check_conv(d, conv_fused(inp, variant="tc3xbf16"), orc.conv_direct_naive(d, x, w, b))

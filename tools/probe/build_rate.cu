@@ -1,0 +1,158 @@
+// Microbenchmark (diagnostics only): cycles of K7's compile-time A producer (3x7x7 stem,
+// stride 2) per tile, with 4 / 8 / 12 producer warps and with / without the TMEM stores.
+#include "../../paper_2407_10730_b200/csrc/conv_ts.cu"
+namespace cb {
+int fail(int code, const std::string&) { return code; }
+int check_launch(const char*) { return 0; }
+int sm_count() { return 148; }
+unsigned long long* debug_trace_buffer(int, cudaStream_t) { return nullptr; }
+}
+using namespace cb;
+
+template <int WARPS, bool ST>
+__global__ void __launch_bounds__(WARPS * 32, 1) build_rate(unsigned long long* out, int iters) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint32_t slot;
+    float* win = reinterpret_cast<float*>(sm);
+    for (int i = threadIdx.x; i < 3 * 11 * 232; i += blockDim.x) win[i] = 0.001f * (i % 997);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) ptx::tmem_alloc(&slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tm = slot;
+    const int quad = warp & 3, kpart = (warp >> 2) % 3;
+    const int m = quad * 32 + lane, ox = m % 112, oy = m / 112;
+    const uint32_t xs = ptx::smem_u32(win) + 4u * (oy * 2 * 232 + ox * 2 + 1);
+    const uint32_t cstride = 4u * 11 * 232, rstride = 4u * 232;
+    const bool swap = lane >= 16;
+    const uint32_t a_hi = tm + ((uint32_t)(quad * 32) << 16) + 128, a_lo = a_hi + 80;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        if (WARPS == 4) {
+            build_fixed_part<3, 7, 7>(0, xs, cstride, rstride, a_hi, a_lo, swap);
+            build_fixed_part<3, 7, 7>(1, xs, cstride, rstride, a_hi, a_lo, swap);
+            build_fixed_part<3, 7, 7>(2, xs, cstride, rstride, a_hi, a_lo, swap);
+        } else if (WARPS == 8) {
+            if (warp < 4) {
+                build_fixed_part<3, 7, 7>(0, xs, cstride, rstride, a_hi, a_lo, swap);
+                build_fixed_part<3, 7, 7>(1, xs, cstride, rstride, a_hi, a_lo, swap);
+            } else {
+                build_fixed_part<3, 7, 7>(2, xs, cstride, rstride, a_hi, a_lo, swap);
+            }
+        } else {
+            build_fixed_part<3, 7, 7>(kpart, xs, cstride, rstride, a_hi, a_lo, swap);
+        }
+        ptx::tmem_st_wait();
+        asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)(t1 - t0));
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc(tm, 512); }
+}
+
+
+// MODE 0: loads + split + stores, 1: loads + split (no stores), 2: stores only, 3: loads only
+template <int MODE>
+__device__ __forceinline__ uint32_t probe_build(uint32_t xs, uint32_t cstride, uint32_t rstride,
+                                                uint32_t a_hi, uint32_t a_lo, bool swap, uint32_t acc) {
+    const uint32_t xa = xs + (swap ? 4u : 0u), xb = xs + (swap ? 0u : 4u);
+#pragma unroll
+    for (int gi = 0; gi < 19; ++gi) {
+        float v[8];
+        if (MODE != 2) {
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) load_pair<3, 7, 7>(gi * 8 + e, xs, xa, xb, cstride, rstride, swap, v[e], v[e + 1]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(acc + e);
+        }
+        uint32_t hv[4], lv[4];
+        if (MODE == 3) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc ^= __float_as_uint(v[e]);
+            continue;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_pair(v[2 * e], v[2 * e + 1], hv[e], lv[e]);
+        if (MODE == 1) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc ^= hv[e] + lv[e];
+        } else {
+            ptx::tmem_st_32x32b_x4(a_hi + gi * 4, hv);
+            ptx::tmem_st_32x32b_x4(a_lo + gi * 4, lv);
+        }
+    }
+    return acc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) build_mode(unsigned long long* out, int iters) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint32_t slot;
+    float* win = reinterpret_cast<float*>(sm);
+    for (int i = threadIdx.x; i < 3 * 11 * 232; i += blockDim.x) win[i] = 0.001f * (i % 997);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) ptx::tmem_alloc(&slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tm = slot;
+    const int m = warp * 32 + lane, ox = m % 112, oy = m / 112;
+    const uint32_t xs = ptx::smem_u32(win) + 4u * (oy * 2 * 232 + ox * 2 + 1);
+    const uint32_t a_hi = tm + ((uint32_t)(warp * 32) << 16) + 128, a_lo = a_hi + 80;
+    uint32_t acc = lane;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        acc = probe_build<MODE>(xs, 4u * 11 * 232, 4u * 232, a_hi, a_lo, lane >= 16, acc);
+        ptx::tmem_st_wait();
+        __syncthreads();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)(t1 - t0));
+    if (acc == 0x12345678u) out[1] = acc;
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc(tm, 512); }
+}
+
+template <int MODE>
+void run_mode(unsigned long long* d) {
+    auto k = build_mode<MODE>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    const int iters = 200;
+    k<<<148, 128, 160 * 1024>>>(d, iters);
+    cudaMemset(d, 0, 8);
+    k<<<148, 128, 160 * 1024>>>(d, iters);
+    unsigned long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    const char* names[] = {"load+split+store", "load+split", "store only", "load only"};
+    printf("4 warps %-18s cycles per tile %.0f  %s\n", names[MODE], (double)h / 148 / iters,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
+template <int WARPS, bool ST>
+void run(unsigned long long* d) {
+    auto k = build_rate<WARPS, ST>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    const int iters = 200;
+    k<<<148, WARPS * 32, 160 * 1024>>>(d, iters);
+    cudaMemset(d, 0, 8);
+    k<<<148, WARPS * 32, 160 * 1024>>>(d, iters);
+    unsigned long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("warps %2d  cycles per tile %.0f  %s\n", WARPS, (double)h / 148 / iters,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+    unsigned long long* d;
+    cudaMalloc(&d, 64);
+    run<4, true>(d);
+    run<8, true>(d);
+    run<12, true>(d);
+    run_mode<0>(d); run_mode<1>(d); run_mode<2>(d); run_mode<3>(d);
+    return 0;
+}
