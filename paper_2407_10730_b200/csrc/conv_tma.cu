@@ -70,6 +70,7 @@ struct TmaParams {
     int64_t full_items;
     int tail_tiles, tail_parts, tail_kbp;
     int64_t total_items;
+    int tail_last;        // diagnostics (CB_TMA_TAIL_LAST): the old order, tail parts last
     int* counters;        // 2 * tail_tiles * CG ([written][done]), self-resetting
     float* partials;      // tail_tiles * tail_parts * CG * BN * 128
     unsigned long long* trace;  // diagnostics (CB_TMA_TRACE): per-CTA globaltimer stamps
@@ -119,9 +120,15 @@ struct WorkItem {
     int part;   // K part of a tail tile
 };
 
+// Item order: the tail parts come FIRST (items [0, tail_items), at most one per cluster, all
+// concurrent), whole tiles after them.  A part's fixup -- park, wait for the other parts,
+// sum its own chunks -- then runs in the epilogue warps while the MMA warp is already on the
+// cluster's next whole tile (the other TMEM accumulator), instead of trailing the kernel.
 __device__ __forceinline__ WorkItem decode_item(const TmaParams& p, int64_t i) {
     WorkItem w;
     int ks;
+    const int64_t tail_items = p.total_items - p.full_items;
+    if (!p.tail_last) i = i < tail_items ? p.full_items + i : i - tail_items;
     if (i < p.full_items) {
         decode_tile(p, i, w.nt, w.mt, w.gi, ks);
         w.kb0 = ks * p.kb_per_split;
@@ -439,37 +446,77 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 __threadfence();
                 // own chunks: all other parts' values of a chunk are loaded before any of its
                 // stores issue (loads never queue behind stores in L1)
+                // Vector stores (PQ % 4 == 0: a group of 4 pixels never straddles an image):
+                // lane l of the epilogue stores pixels m0 + 4l .. + 3 of channel rows.
+                const bool vec_store = (g.PQ % 4) == 0 && !(p.debug & 2);
+                const int64_t jv = it.mt * (TMA_BM * CG) + rank * TMA_BM + 4 * lane;
+                const bool gvalid = jv < g.npix;
+                float* vbase = p.out;
+                if (vec_store && gvalid) {
+                    const int64_t nv = jv / g.PQ;
+                    vbase += nv * (int64_t)g.K * g.PQ + (jv - nv * g.PQ) + (int64_t)(gi * g.kpg + f_tile0) * g.PQ;
+                }
 #pragma unroll 1
                 for (int ci = own_lo; ci < own_hi; ++ci) {
                     const int c0 = ci * 32;
                     const int nvalid = min(32, g.kpg - (f_tile0 + c0));
                     uint32_t r[32];
                     ptx::tmem_ld_32x32b_x32(lane_tm + c0, r);
-                    float v[32];
+                    // every other part's values of the chunk in flight at once (one L2
+                    // round trip per chunk), then the sum in part order
+                    float4 pv[MAX_TAIL_OTHERS + 1][8];  // indexed by part (own slot unused)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
-                    for (int q = 0; q < P; ++q) {  // sum over parts in part order
-                        if (q == it.part) {
-                            ptx::tmem_ld_wait();
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
-                        } else {
+                    for (int q = 0; q <= MAX_TAIL_OTHERS; ++q) {
+                        if (q < P && q != it.part) {
                             const float4* src = reinterpret_cast<const float4*>(
                                                     slab_of + (int64_t)q * CG * slab) +
                                                 (int64_t)(ci * 8) * TMA_BM + row;
-                            float4 pv[8];
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) pv[j] = __ldcg(src + (int64_t)j * TMA_BM);
+                            for (int j = 0; j < 8; ++j) pv[q][j] = __ldcg(src + (int64_t)j * TMA_BM);
+                        }
+                    }
+                    ptx::tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+#pragma unroll
+                    for (int q = 0; q <= MAX_TAIL_OTHERS; ++q) {  // sum over parts in part order
+                        if (q >= P) break;
+                        if (q == it.part) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
+                        } else {
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                v[4 * j] += pv[j].x;
-                                v[4 * j + 1] += pv[j].y;
-                                v[4 * j + 2] += pv[j].z;
-                                v[4 * j + 3] += pv[j].w;
+                                v[4 * j] += pv[q][j].x;
+                                v[4 * j + 1] += pv[q][j].y;
+                                v[4 * j + 2] += pv[q][j].z;
+                                v[4 * j + 3] += pv[q][j].w;
                             }
                         }
                     }
-                    if (do_store) {
+                    if (vec_store) {
+                        // transpose through shared memory so each lane stores 4 consecutive
+                        // pixels of one channel: a warp writes a 512-byte channel row per
+                        // STG.128 instead of a 128-byte one per STG.32
+                        float* buf = ostage + (ochunk & 1) * (32 * TMA_BM);
+                        ++ochunk;
+                        if (threadIdx.x == 0) ptx::bulk_wait_read<0>();  // no TMA store reads buf
+                        epi_barrier();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            buf[i * TMA_BM + row] = v[i] + (bias && i < nvalid ? __ldg(bias + c0 + i) : 0.f);
+                        epi_barrier();
+                        if (gvalid) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int ch = quad + 4 * q;
+                                if (ch < nvalid)
+                                    *reinterpret_cast<float4*>(vbase + (int64_t)(c0 + ch) * g.PQ) =
+                                        *reinterpret_cast<const float4*>(buf + ch * TMA_BM + 4 * lane);
+                            }
+                        }
+                    } else if (do_store) {
                         float* d = dst + (int64_t)c0 * g.PQ;
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -953,6 +1000,7 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     prm.total_tiles = pl.total_tiles;
     prm.full_items = pl.full_items;
     prm.total_items = pl.total_items;
+    prm.tail_last = std::getenv("CB_TMA_TAIL_LAST") ? 1 : 0;
     prm.tail_tiles = pl.tail_tiles;
     prm.tail_parts = pl.tail_parts;
     prm.tail_kbp = pl.tail_kbp;
