@@ -13,7 +13,12 @@
 // written once: algorithmic bytes = 4 * (N*C*H*W + C*R*S*N*P*Q).
 #include <algorithm>
 
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "cb_common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace cb {
 
@@ -114,22 +119,33 @@ struct BandPlan {
     int IR, IWp;       // staged window rows / row pitch
     int bands_per_unit;  // bands per image (K1) or per slice (K2)
     int PXT;             // pixels of a full band (offset-table size)
+    // TMA staging: the window is one 4-D box {IWp, IR, CC, 1} of x loaded at column -x0
+    // (x0 = pw rounded up to 4: 16-byte aligned start), zero-filled outside the tensor;
+    // window column = input column + x0.  0: per-element loads, column = input col + pw.
+    int tma, x0;
+    // NB > 1 (K1 with TMA, whole-image bands of small images): a block packs NB consecutive
+    // images -- one box {IWp, IR, CC, NB} -- so each packed row run is NB * P * Q pixels
+    int NB;
     size_t smem;
 };
 
 template <bool SLICED>
 __global__ void __launch_bounds__(BAND_THREADS)
 im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __restrict__ out,
-                   int band_rows, int first_slice, int64_t j_begin) {
-    extern __shared__ float smem_band[];  // [pixel offset table][CC][IR][IWp]
-    int* off_tab = reinterpret_cast<int*>(smem_band);
-    float* win = smem_band + (bp.PXT + 3) / 4 * 4;
+                   int band_rows, int first_slice, int64_t j_begin,
+                   const __grid_constant__ CUtensorMap tm_x) {
+    extern __shared__ __align__(128) float smem_band[];  // [CC][IR][IWp][pixel tab][row tab]
+    __shared__ __align__(8) uint64_t win_bar;
+    float* win = smem_band;
+    int* off_tab = reinterpret_cast<int*>(smem_band + (size_t)bp.NB * bp.CC * bp.IR * bp.IWp);
     // ---- which band ----
     const int unit = blockIdx.x / bp.bands_per_unit;  // image (K1) or slice index (K2)
     const int sub = blockIdx.x - unit * bp.bands_per_unit;
     int n, y_lo, y_hi;  // output rows [y_lo, y_hi) of image n
+    int nb = 1;  // images of this block (NB > 1: whole-image bands, y_lo = 0)
     if (!SLICED) {
-        n = unit;
+        n = unit * bp.NB;
+        nb = min(bp.NB, g.N - n);
         y_lo = sub * bp.TR;
         y_hi = min(g.P, y_lo + bp.TR);
     } else {
@@ -144,14 +160,22 @@ im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __re
     if (y_lo >= y_hi) return;  // block-uniform
     const int c0 = blockIdx.y * bp.CC;
     const int cc = min(bp.CC, g.C - c0);
-    const int npx = (y_hi - y_lo) * g.Q;
+    const int npx = nb * (y_hi - y_lo) * g.Q;
     const int iy0 = y_lo * g.sh - g.ph;
     const int ir = (y_hi - y_lo - 1) * g.sh + (g.R - 1) * g.dh + 1;
     // ---- stage the zero-padded window [cc][ir][IWp] (this band's own row count, so the
     //      smem index of element e is e); (c, r, col) advance by counters, no division ----
     const float* xb = x + ((int64_t)n * g.C + c0) * g.HW;
     const int tot = cc * ir * bp.IWp;
-    {
+    const int wrows = bp.tma ? bp.IR : ir;  // window plane rows (the TMA box is always full)
+    if (bp.tma) {
+        if (threadIdx.x == 0) {
+            ptx::mbar_init(&win_bar, 1);
+            ptx::fence_mbar_init();
+            ptx::mbar_arrive_expect_tx(&win_bar, (uint32_t)(bp.NB * bp.CC * bp.IR * bp.IWp * 4));
+            ptx::tma_load_4d(win, &tm_x, &win_bar, -bp.x0, iy0, c0, n);  // NB images: box dim 3
+        }
+    } else {
         const int plane = ir * bp.IWp;
         // BAND_THREADS in the mixed radix (c, r, col) = (., ir, IWp)
         const int drow = BAND_THREADS / bp.IWp, dcol = BAND_THREADS - drow * bp.IWp;
@@ -183,19 +207,25 @@ im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __re
     }
     // ---- pixel -> window offset table (the same for every packed row of the band) and
     //      packed row -> window base table (no integer division in the store loop) ----
-    int* row_tab = off_tab + (bp.PXT + 3) / 4 * 4 + bp.CC * bp.IR * bp.IWp;
+    int* row_tab = off_tab + (bp.PXT + 3) / 4 * 4;
+    const int col0 = bp.tma ? bp.x0 - g.pw : 0;  // window column of the band's first tap
+    const int bpx = (y_hi - y_lo) * g.Q;                   // pixels per image of the band
+    const int img_words = bp.CC * bp.IR * bp.IWp;          // window words per image (NB > 1)
     for (int pix = threadIdx.x; pix < npx; pix += BAND_THREADS) {
-        const int oyl = pix / g.Q;
-        off_tab[pix] = oyl * g.sh * bp.IWp + (pix - oyl * g.Q) * g.sw;
+        const int b = bp.NB > 1 ? pix / bpx : 0;
+        const int pl = pix - b * bpx;
+        const int oyl = pl / g.Q;
+        off_tab[pix] = b * img_words + oyl * g.sh * bp.IWp + (pl - oyl * g.Q) * g.sw + col0;
     }
     const int nrows = cc * g.RS;
     for (int r = threadIdx.x; r < nrows; r += BAND_THREADS) {
         const int c = r / g.RS;
         const int t = r - c * g.RS;
         const int ky = t / g.S, kx = t - (t / g.S) * g.S;
-        row_tab[r] = (c * ir + ky * g.dh) * bp.IWp + kx * g.dw;
+        row_tab[r] = (c * wrows + ky * g.dh) * bp.IWp + kx * g.dw;
     }
     __syncthreads();
+    if (bp.tma) ptx::mbar_wait(&win_bar, 0);
     // ---- destination of this band's run in every packed row ----
     const int64_t jband = (int64_t)n * g.PQ + (int64_t)y_lo * g.Q;
     int64_t row_stride, dst0;
@@ -248,7 +278,7 @@ im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __re
 }
 
 // Band geometry: ~1-2K pixels per band (<= BAND_THREADS * BAND_MAXM), window <= 40 KB.
-static bool band_plan(const Geom& g, int max_rows, int64_t units, BandPlan* bp) {
+static bool band_plan(const Geom& g, int max_rows, int64_t units, BandPlan* bp, bool multi_image) {
     const int cap_px = BAND_THREADS * BAND_MAXM;
     if (g.Q > cap_px) return false;
     int tr = std::max(1, std::min(max_rows, 1536 / std::max(1, g.Q)));
@@ -273,12 +303,36 @@ static bool band_plan(const Geom& g, int max_rows, int64_t units, BandPlan* bp) 
     bp->TR = tr;
     bp->IR = (tr - 1) * g.sh + (g.R - 1) * g.dh + 1;
     bp->IWp = g.W + 2 * g.pw;
-    const size_t per_ch = per_ch_of(tr);
+    bp->tma = 0;
+    bp->x0 = 0;
+    {
+        const int x0 = (g.pw + 3) / 4 * 4;
+        const int bw = (g.W + g.pw + x0 + 3) / 4 * 4;
+        static const bool no_tma = getenv("CB_BAND_NO_TMA") != nullptr;
+        if (!no_tma && g.W % 4 == 0 && bw <= 256 && bp->IR <= 256 && cc <= 256) {
+            bp->tma = 1;
+            bp->x0 = x0;
+            bp->IWp = bw;
+        }
+    }
+    const size_t per_ch = (size_t)bp->IR * bp->IWp * sizeof(float);
     if (per_ch > 96 * 1024) return false;
+    bp->NB = 1;
+    // (measured neutral on cfg4, so off unless CB_BAND_NB is set)
+    static const bool use_nb = getenv("CB_BAND_NB") != nullptr;
+    if (multi_image && use_nb && bp->tma && tr == max_rows && g.PQ < 1024 && g.N > 1) {
+        // runs of >= ~1K pixels; the window budget is shared by the NB images
+        bp->NB = (int)std::min<int64_t>(std::min(g.N, 256), (1024 + g.PQ - 1) / g.PQ);
+        cc = (int)std::max<size_t>(1, std::min<size_t>(cc, (16 * 1024) / (per_ch * bp->NB)));
+    }
     bp->CC = cc;
-    bp->PXT = tr * g.Q;  // offset-table entries (pixels of a full band)
-    bp->smem = per_ch * bp->CC + sizeof(int) * ((bp->PXT + 3) / 4 * 4) +
+    bp->PXT = bp->NB * tr * g.Q;  // offset-table entries (pixels of a full band)
+    bp->smem = per_ch * bp->CC * bp->NB + sizeof(int) * ((bp->PXT + 3) / 4 * 4) +
                sizeof(int) * (size_t)bp->CC * g.RS;
+    if (bp->smem > 200 * 1024) {  // (tiny channel groups never get here)
+        bp->tma = 0;
+        bp->NB = 1;
+    }
     return true;
 }
 
@@ -286,11 +340,32 @@ int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, i
                        int first_slice, int count, int64_t j_begin, cudaStream_t st) {
     BandPlan bp{};
     const int64_t units = sliced ? count : g.N;
-    if (!band_plan(g, sliced ? band_rows : g.P, units, &bp)) return CB_ERR_UNSUPPORTED;
+    if (!band_plan(g, sliced ? band_rows : g.P, units, &bp, !sliced)) return CB_ERR_UNSUPPORTED;
     bp.bands_per_unit = ((sliced ? band_rows : g.P) + bp.TR - 1) / bp.TR;
-    const int64_t gx = units * bp.bands_per_unit;
+    const int64_t gx = (units + bp.NB - 1) / bp.NB * bp.bands_per_unit;
     const int64_t gy = (g.C + bp.CC - 1) / bp.CC;
     if (gx > 0x7fffffffLL || gy > 65535) return CB_ERR_UNSUPPORTED;
+    CUtensorMap tm{};
+    if (bp.tma && (reinterpret_cast<uintptr_t>(x) & 15)) bp.tma = 0;
+    if (bp.tma) {
+        static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+        static std::once_flag once;
+        std::call_once(once, [] {
+            void* ptr = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                    cudaSuccess && q == cudaDriverEntryPointSuccess)
+                enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        });
+        cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.C, (cuuint64_t)g.N};
+        cuuint64_t strides[3] = {(cuuint64_t)g.W * 4, (cuuint64_t)g.HW * 4, (cuuint64_t)g.C * g.HW * 4};
+        cuuint32_t box[4] = {(cuuint32_t)bp.IWp, (cuuint32_t)bp.IR, (cuuint32_t)bp.CC, (cuuint32_t)bp.NB};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (!enc || enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (band window) failed");
+    }
     auto kern = sliced ? im2col_band_kernel<true> : im2col_band_kernel<false>;
     if (bp.smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -298,7 +373,7 @@ int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, i
         if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
     }
     kern<<<dim3((unsigned)gx, (unsigned)gy), BAND_THREADS, bp.smem, st>>>(
-        g, bp, x, out, band_rows, first_slice, j_begin);
+        g, bp, x, out, band_rows, first_slice, j_begin, tm);
     return check_launch(sliced ? "sconv_pack_band" : "im2col_band");
 }
 
