@@ -49,6 +49,9 @@ struct TsParams {
     int x0;                 // window column 0 = input column -x0 (x0 = pw rounded up to 4)
     uint32_t stage_bytes;   // C * box_rows * box_w * 4 (TMA transaction bytes)
     uint32_t stage_stride;  // stage_bytes rounded to 1 KB (buffer pitch)
+    int nwin;               // staging windows in the ring (2..4): the window TMA of tile i +
+                            // nwin - 1 is in flight while tile i is built (its L2 latency,
+                            // ~2.6k cycles on cfg3, exceeds one tile's A build)
     uint32_t w_half_bytes;  // n_pad * kb_w * 2
     int debug;              // diagnostics (CB_TS_DEBUG): 1 no MMA, 2 no tcgen05.st, 4 no input TMA
     int tma_store;          // 1: epilogue stages 32-channel chunks in smem, TMA stores them
@@ -207,17 +210,17 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     uint8_t* w_hi = smem;
     uint8_t* w_lo = smem + p.w_half_bytes;
     float* stage0 = reinterpret_cast<float*>(smem + 2 * p.w_half_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * p.w_half_bytes + 2 * p.stage_stride);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * p.w_half_bytes + p.nwin * p.stage_stride);
     uint64_t* w_full = bars;            // 1
-    uint64_t* s_full = bars + 1;        // 2: staging window landed
-    uint64_t* s_empty = bars + 3;       // 2: producers done with the window
-    uint64_t* a_full = bars + 5;        // 2: A buffer written
-    uint64_t* a_empty = bars + 7;       // 2: MMAs done reading the A buffer
-    uint64_t* acc_full = bars + 9;      // 2: accumulator ready
-    uint64_t* acc_empty = bars + 11;    // 2: epilogue drained the accumulator
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+    uint64_t* s_full = bars + 1;        // 4: staging window landed
+    uint64_t* s_empty = bars + 5;       // 4: producers done with the window
+    uint64_t* a_full = bars + 9;        // 2: A buffer written
+    uint64_t* a_empty = bars + 11;      // 2: MMAs done reading the A buffer
+    uint64_t* acc_full = bars + 13;     // 2: accumulator ready
+    uint64_t* acc_empty = bars + 15;    // 2: epilogue drained the accumulator
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
     // epilogue staging: 2 x [32 channels][128 pixels] fp32 (after the barriers, 1 KB aligned)
-    float* ostage = reinterpret_cast<float*>(smem + 2 * p.w_half_bytes + 2 * p.stage_stride + 1024);
+    float* ostage = reinterpret_cast<float*>(smem + 2 * p.w_half_bytes + p.nwin * p.stage_stride + 1024);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -227,9 +230,11 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(w_full, 1);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < p.nwin; ++b) {
             ptx::mbar_init(&s_full[b], 1);
             ptx::mbar_init(&s_empty[b], 32 * TS_PROD_WARPS);
+        }
+        for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&a_full[b], 32 * TS_PROD_WARPS);
             ptx::mbar_init(&a_empty[b], 1);
             ptx::mbar_init(&acc_full[b], 1);
@@ -273,6 +278,8 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         const int nchunks = p.kp / 32;
         const bool swap = (g.sw % 2 == 0) && lane >= 16 && !(p.debug & 32);
         int i = 0;
+        int ws = 0;  // staging-window ring slot and phase
+        uint32_t wph = 0;
         for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
@@ -282,9 +289,9 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
             const int oy = div_q(pix, p);
             const int ox = pix - oy * g.Q;
-            const uint32_t xs = ptx::smem_u32(stage0) + b * p.stage_stride +
+            const uint32_t xs = ptx::smem_u32(stage0) + ws * p.stage_stride +
                                 4u * (uint32_t)((oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw));
-            ptx::mbar_wait(&s_full[b], ph);
+            ptx::mbar_wait(&s_full[ws], wph);
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 1 : 11, i);
             ptx::mbar_wait(&a_empty[b], ph ^ 1);
             ptx::tc_fence_after();
@@ -334,7 +341,11 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             ptx::tc_fence_before();
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 4 : 14, i);
             ptx::mbar_arrive(&a_full[b]);
-            ptx::mbar_arrive(&s_empty[b]);
+            ptx::mbar_arrive(&s_empty[ws]);
+            if (++ws == p.nwin) {
+                ws = 0;
+                wph ^= 1;
+            }
         }
     } else if (warp < TS_TMA_WARP) {
         // ============================ epilogue ==========================================
@@ -414,22 +425,28 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         }
         __syncwarp();
         int i = 0;
+        int ws = 0;  // staging-window ring slot and phase
+        uint32_t wph = 0;
         for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const int n = tw.n;
             const int p0 = tw.ti * TS_BM;
             const int iy0 = div_q(p0, p) * g.sh - g.ph;
-            ptx::mbar_wait(&s_empty[b], ph ^ 1);
+            ptx::mbar_wait(&s_empty[ws], wph ^ 1);
             if (leader) ts_stamp(p, 0, i);
             if (leader && (p.debug & 4)) {
-                ptx::mbar_arrive(&s_full[b]);
+                ptx::mbar_arrive(&s_full[ws]);
             } else if (leader) {
-                ptx::mbar_arrive_expect_tx(&s_full[b], p.stage_bytes);
-                ptx::tma_load_4d(reinterpret_cast<uint8_t*>(stage0) + (size_t)b * p.stage_stride, &tm_x,
-                                 &s_full[b], -p.x0, iy0, 0, n);
+                ptx::mbar_arrive_expect_tx(&s_full[ws], p.stage_bytes);
+                ptx::tma_load_4d(reinterpret_cast<uint8_t*>(stage0) + (size_t)ws * p.stage_stride, &tm_x,
+                                 &s_full[ws], -p.x0, iy0, 0, n);
             }
             __syncwarp();
+            if (++ws == p.nwin) {
+                ws = 0;
+                wph ^= 1;
+            }
         }
     } else {
         // ============================ MMA issuer ========================================
@@ -482,6 +499,7 @@ struct TsPlan {
     bool ok;
     int kp, n_pad, kb_w, box_rows, box_w, x0;
     uint32_t stage_bytes, stage_stride, w_half_bytes;
+    int nwin;
     bool tma_store;
     size_t smem;
 };
@@ -514,9 +532,18 @@ static TsPlan plan_ts(const Geom& g) {
     pl.w_half_bytes = (uint32_t)pl.n_pad * pl.kb_w * 2;
     // >= 120 KB keeps one CTA per SM (each allocates all 512 TMEM columns)
     pl.tma_store = (g.PQ % 4) == 0;  // 16-byte global strides for the output map
-    pl.smem = std::max<size_t>(120 * 1024, 1024 + 2 * (size_t)pl.w_half_bytes +
-                                               2 * (size_t)pl.stage_stride + 1024 +
-                                               2 * 32 * TS_BM * 4 + 4 * (size_t)pl.kp);
+    auto smem_for = [&](int nwin) {
+        return std::max<size_t>(120 * 1024, 1024 + 2 * (size_t)pl.w_half_bytes +
+                                                nwin * (size_t)pl.stage_stride + 1024 +
+                                                2 * 32 * TS_BM * 4 + 4 * (size_t)pl.kp);
+    };
+    static const int max_win = [] {
+        const char* e = std::getenv("CB_TS_NWIN");
+        return e ? std::max(2, std::min(4, std::atoi(e))) : 4;
+    }();
+    pl.nwin = 2;
+    while (pl.nwin < max_win && smem_for(pl.nwin + 1) <= 227 * 1024) ++pl.nwin;
+    pl.smem = smem_for(pl.nwin);
     pl.ok = pl.stage_bytes <= 64 * 1024 && pl.smem <= 227 * 1024;
     return pl;
 }
@@ -621,6 +648,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.x0 = pl.x0;
     prm.stage_bytes = pl.stage_bytes;
     prm.stage_stride = pl.stage_stride;
+    prm.nwin = pl.nwin;
     prm.w_half_bytes = pl.w_half_bytes;
     if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
     if (std::getenv("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);

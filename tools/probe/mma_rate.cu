@@ -55,7 +55,19 @@ __global__ void __launch_bounds__(192, 1) mma_rate(unsigned long long* out) {
         unsigned long long n = 0;
         const uint32_t lane_base = tm + ((uint32_t)(warp * 32) << 16);
         while (!*done) {
-            if (SIDE == 1) {
+            if (SIDE == 3) {
+                const uint32_t base = ptx::smem_u32(a_s) + 4 * (threadIdx.x & 31);
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    uint32_t v;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 128 * q));
+                    r[q] ^= v;
+                }
+            } else if (SIDE == 4) {
+                const uint32_t base = ptx::smem_u32(b_s) + 16384 + 4 * (threadIdx.x & 31);
+#pragma unroll
+                for (int q = 0; q < 32; ++q) asm volatile("st.shared.u32 [%0], %1;" ::"r"(base + 128 * (q & 7)), "r"(r[q]));
+            } else if (SIDE == 1) {
                 ptx::tmem_ld_32x32b_x32(lane_base + (n & 1) * 32, r);
                 ptx::tmem_ld_wait();
             } else {
@@ -65,6 +77,7 @@ __global__ void __launch_bounds__(192, 1) mma_rate(unsigned long long* out) {
             ++n;
         }
         if (threadIdx.x == 0) atomicAdd(out + 2 + 0 * blockIdx.x, n);
+        if (r[0] == 0x12345u) out[3] = r[1];
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -87,7 +100,7 @@ void run(unsigned long long* d) {
     const double cyc = (double)h[1] / 148 / ITER;
     const double side_bytes = SIDE ? (double)h[2] * 16384.0 / (double)h[1] : 0;  // per SM per cycle
     printf("%s N=%3d side=%s  cycles/MMA %.1f  (block0 %.1f)  floor %d  side B/cyc %.1f  %s\n", TS ? "TS" : "SS", N,
-           SIDE == 0 ? "none" : SIDE == 1 ? "ld  " : "st  ", cyc, (double)h[0] / ITER, 128 * N / 256, side_bytes,
+           SIDE == 0 ? "none" : SIDE == 1 ? "ld  " : SIDE == 2 ? "st  " : SIDE == 3 ? "LDS " : "STS ", cyc, (double)h[0] / ITER, 128 * N / 256, side_bytes,
            e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
@@ -100,5 +113,6 @@ int main() {
     run<1, 64, 1>(d); run<1, 64, 2>(d);
     run<1, 128, 1>(d); run<1, 128, 2>(d);
     run<0, 64, 1>(d); run<0, 64, 2>(d);
+    run<1, 64, 3>(d); run<1, 64, 4>(d); run<1, 128, 3>(d); run<0, 64, 3>(d);
     return 0;
 }
