@@ -77,16 +77,24 @@ def test_fused_tail_split(cuda, cg, monkeypatch):
     from paper_2407_10730_b200.algos import conv_fused, fused_plan
     from paper_2407_10730_b200.descriptor import ConvDescriptor
     monkeypatch.setenv("CB_TMA_CG", str(cg))
-    d = ConvDescriptor(batch=80, in_channels=64, in_h=16, in_w=16, out_channels=64, k_h=3,
-                       k_w=3, pad_h=1, pad_w=1, has_bias=True)
-    inp, (x, w, b) = _inputs(d)
-    ref = orc.conv_im2col64(d, x, w, b)
-    y1 = conv_fused(inp)
-    y2 = conv_fused(inp)
-    _check_conv(d, y1, ref)
-    assert np.array_equal(y1, y2), "tail fixup must be deterministic"
-    monkeypatch.setenv("CB_TMA_TAIL", "0")
-    _check_conv(d, conv_fused(inp), ref)
+    # PQ % 4 == 0 (vector fixup stores through a smem transpose) and PQ odd (direct stores)
+    for hw in (16, 15):
+        monkeypatch.delenv("CB_TMA_TAIL", raising=False)
+        monkeypatch.delenv("CB_TMA_TAIL_LAST", raising=False)
+        d = ConvDescriptor(batch=80, in_channels=64, in_h=hw, in_w=hw, out_channels=64, k_h=3,
+                           k_w=3, pad_h=1, pad_w=1, has_bias=True)
+        assert fused_plan(d)["m_tiles"] > 0
+        inp, (x, w, b) = _inputs(d)
+        ref = orc.conv_im2col64(d, x, w, b)
+        y1 = conv_fused(inp)
+        y2 = conv_fused(inp)
+        _check_conv(d, y1, ref)
+        assert np.array_equal(y1, y2), "tail fixup must be deterministic"
+        # tail parts last (the old item order): the same sums in the same order, same bits
+        monkeypatch.setenv("CB_TMA_TAIL_LAST", "1")
+        assert np.array_equal(conv_fused(inp), y1)
+        monkeypatch.setenv("CB_TMA_TAIL", "0")
+        _check_conv(d, conv_fused(inp), ref)
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
