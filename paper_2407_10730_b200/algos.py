@@ -679,6 +679,22 @@ class FusedConv:
                 y_dev.data_ptr(), st))
         return y_dev
 
+    def capture_steps(self, steps, bias_dev=None):
+        """One CUDA graph of several full steps in sequence, `steps` = [(x, w, y), ...]:
+        a stream of convolutions replayed with one graph launch (no inter-graph gaps)."""
+        torch = _torch()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside capture (attributes, tensor maps)
+            for x_dev, w_dev, y_dev in steps:
+                self.run(x_dev, y_dev, bias_dev, weights=w_dev)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for x_dev, w_dev, y_dev in steps:
+                self.run(x_dev, y_dev, bias_dev, weights=w_dev)
+        return graph
+
     def capture(self, x_dev, w_dev, y_dev, bias_dev=None, ledger=None):
         """CUDA graph of one full step (K3 + K0 + K6) bound to these buffers.  A ledger
         built with EventLedger(external=True) is captured too: every replay re-records its
