@@ -51,7 +51,17 @@ struct G8Params {
     int tma_a;        // 1: A chunks arrive by TMA into smem, 0: per-thread loads
     int tps;          // > 0: SConv slices, tiles never cross a slice: tps tiles per slice of np px
     int np;
+    // Tail N-split: items [0, full_items) are whole tiles; each of the remaining tiles (the
+    // ragged last wave) is cut into tail_split channel ranges (multiples of 16 columns), one
+    // item each, so the last wave keeps every SM busy.  A is rebuilt per range.
+    int64_t full_items;
+    int tail_split;
 };
+
+// channel range [lo, hi) of part `sub` of a BN-wide tile cut into `parts` (16-aligned)
+__device__ __forceinline__ int g8_part_col(int bn, int parts, int sub) {
+    return min(bn, ((bn * sub / parts) + 15) / 16 * 16);
+}
 
 template <int BN, bool BF16>
 struct G8Cfg {
@@ -129,8 +139,18 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         jl = mt * G8_BM + m;
         return jl < p.pm.j_count;
     };
-    // item -> (channel tile nt, pixel tile mt, group gi)
+    // item -> (channel tile nt, pixel tile mt, group gi; tile columns [c_lo, c_hi))
+    int c_lo = 0, c_hi = BN;
     auto decode = [&](int64_t t, int& nt, int64_t& mt, int& gi) {
+        c_lo = 0;
+        c_hi = BN;
+        if (t >= p.full_items) {
+            const int64_t j = t - p.full_items;
+            const int sub = (int)(j % p.tail_split);
+            t = p.full_items + j / p.tail_split;
+            c_lo = g8_part_col(BN, p.tail_split, sub);
+            c_hi = g8_part_col(BN, p.tail_split, sub + 1);
+        }
         nt = (int)(t % p.n_tiles);
         const int64_t r = t / p.n_tiles;
         mt = r % p.m_tiles;
@@ -220,10 +240,10 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             const bool jvalid = pix_of(mt, m, jl);
             int64_t obase = 0, ostride = 0;
             if (jvalid) dst_linear(g, p.pm, p.pm.j_begin + jl, obase, ostride);
-            const int f_tile0 = nt * BN;
+            const int f_tile0 = nt * BN + c_lo;
             ptx::mbar_wait(acc_full, i & 1);
             ptx::tc_fence_after();
-            const int ncol = min(BN, g.kpg - f_tile0);
+            const int ncol = min(c_hi - c_lo, g.kpg - f_tile0);
 #pragma unroll 1
             for (int c0 = 0; c0 < ncol; c0 += 32) {
                 uint32_t r[32];
@@ -289,7 +309,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
-            const int row0 = gi * g.kpg + nt * BN;
+            const int row0 = gi * g.kpg + nt * BN + c_lo;  // (a part's rows start the stage)
             for (int kb = 0; kb < nstage; ++kb) {
                 const int64_t sg = sbase + kb;
                 const int s = (int)(sg % p.bstages);
@@ -307,13 +327,18 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
     } else {
         // ============================ MMA issuer ========================================
         const uint32_t leader = ptx::elect_one();
-        constexpr uint32_t idesc = ptx::idesc_f32acc<BF16>(G8_BM, BN);
+        constexpr uint32_t idesc_full = ptx::idesc_f32acc<BF16>(G8_BM, BN);
         const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(smem));
         constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
         const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
         int64_t cbase = 0, sbase = 0;
         int i = 0;
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++i, cbase += nch, sbase += nstage) {
+            int nt, gi;
+            int64_t mt;
+            decode(t, nt, mt, gi);
+            const uint32_t idesc =
+                c_hi - c_lo == BN ? idesc_full : ptx::idesc_f32acc<BF16>(G8_BM, c_hi - c_lo);
             ptx::mbar_wait(acc_empty, (i & 1) ^ 1);
             ptx::tc_fence_after();
             for (int kc = 0; kc < nch; ++kc) {
@@ -459,6 +484,21 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
     // (narrower channel tiles for short grids measured slower: A is rebuilt per channel tile)
     prm.n_tiles = (g.kpg + bn - 1) / bn;
     prm.items = prm.m_tiles * prm.n_tiles * g.G;
+    prm.full_items = prm.items;
+    prm.tail_split = 1;
+    {
+        const int64_t grid = std::min<int64_t>(prm.items, sm_count());
+        const int64_t tail = prm.items % grid;
+        static const bool no_split = std::getenv("CB_K8_NO_TAIL_SPLIT") != nullptr;
+        if (!no_split && prm.items > grid && tail > 0) {
+            const int parts = (int)std::min<int64_t>(std::min<int64_t>(grid / tail, 4), bn / 32);
+            if (parts >= 2) {
+                prm.full_items = prm.items - tail;
+                prm.tail_split = parts;
+                prm.items = prm.full_items + tail * parts;
+            }
+        }
+    }
     prm.tma_a = pm.src_mode == SRC_MATRIX && (pm.src_ld % 4) == 0 &&
                 (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pm.j_begin + pm.j_count <= pm.src_ld &&
                 !std::getenv("CB_K8_NO_TMA_A");
