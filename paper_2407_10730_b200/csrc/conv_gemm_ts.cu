@@ -471,7 +471,8 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
     prm.out = out;
     prm.add_mode = add_mode;
     prm.nchunks = (g.kdim + G8_CK - 1) / G8_CK;
-    const int bn = g.kpg <= 64 ? 64 : g.kpg <= 128 ? 128 : 256;
+    int bn = g.kpg <= 64 ? 64 : g.kpg <= 128 ? 128 : 256;
+    if (const char* e = std::getenv("CB_K8_BN")) bn = std::min(bn, std::max(64, std::atoi(e)));  // diagnostics
     prm.m_tiles = (pm.j_count + G8_BM - 1) / G8_BM;
     const bool slice_tma = pm.src_mode == SRC_SLICES && pm.band_rows > 0 &&
                            g.P % pm.band_rows == 0 && (pm.band_rows * g.Q) % 4 == 0 &&
