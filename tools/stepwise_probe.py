@@ -2,6 +2,10 @@
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import os
+if os.environ.get("CB_LIB_PATH"):  # A/B runs against another build
+    from paper_2407_10730_b200 import _capi as _c
+    _c.LIB_PATH = Path(os.environ["CB_LIB_PATH"])
 import torch
 from paper_2407_10730_b200 import algos
 from paper_2407_10730_b200.configs import CONFIGS
