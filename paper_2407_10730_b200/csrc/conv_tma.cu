@@ -759,7 +759,7 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     best.m_tiles = ceil_div64(g.npix, TMA_BM);
     best.n_tiles = (g.kpg + 63) / 64;
     double best_cost = 1e300;
-    for (int cg : {2, 1}) {
+    for (int cg : {1, 2}) {  // ties go to single CTAs (no pair sync; measured faster on cfg1)
         if (force_cg && std::atoi(force_cg) != cg) continue;
         for (int bn : {256, 128, 64}) {
             if (force_bn && std::atoi(force_bn) != bn) continue;
@@ -815,6 +815,11 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
         const int min_kbp = tiles > units ? 4 : 2;
         int parts = (int)std::min<int64_t>(std::min<int64_t>(units / tail, L.num_kb / min_kbp),
                                            MAX_TAIL_OTHERS + 1);
+        // the fixup (park, publish, wait, sum) costs ~2-3 us: split only when the MMA time it
+        // takes off a tail tile is larger (cfg1 / cfg2b: 9.7 -> 8.3 / 8.7 -> 6.3 us unsplit)
+        const double tile_mma = 12.0 * L.num_kb * (pl.bn / 2.0);  // cycles, as in the model
+        if (parts >= 2 && tile_mma * (1.0 - 1.0 / parts) < 4000.0 && !std::getenv("CB_TMA_TAIL_ALWAYS"))
+            parts = 1;
         if (parts >= 2) {
             pl.tail_kbp = (L.num_kb + parts - 1) / parts;
             parts = (L.num_kb + pl.tail_kbp - 1) / pl.tail_kbp;
@@ -943,16 +948,18 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
     // programmatic dependent launch: the prologue (barriers, TMEM, descriptor prefetch)
     // overlaps the tail of the preceding kernel (K0); griddepcontrol.wait guards the inputs
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = std::getenv("CB_NO_PDL") ? 0 : 1;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("CB_NO_PDL") ? 0 : 1;
+    // cluster dimension only for CTA pairs (a 1-CTA cluster launch measured ~12% slower on
+    // the stepwise GEMM)
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CG;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = CG == 2 ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mah, mal, mwh, mwl, my);
     if (e != cudaSuccess) return fail(CB_ERR_CUDA, std::string("conv_tma launch: ") + cudaGetErrorString(e));
     return check_launch("conv_tma_kernel");
