@@ -167,3 +167,20 @@ def test_fused_layout_paths(lib):
     assert algos.resolve_variant(CONFIGS["cfg1"], "auto") == "tc3xbf16"
     assert algos.resolve_variant(CONFIGS["cfg2a"], "auto") == "ffma"
     assert algos.resolve_variant(CONFIGS["cfg4"], "tc3xtf32") == "tc3xtf32"
+
+
+def test_fused_tile_plans(lib):
+    """K6 tile plans (cb_fused_plan_tiles, host arithmetic; 148 SMs assumed without a GPU):
+    CTA pairs with a tail split on the big grid (cfg4: 98 pair tiles on 74 pairs, the 24 tail
+    tiles in 3 K parts -> 74 + 72 items on 148 CTAs), single CTAs and no split on short grids
+    whose tiles are too short for the fixup to pay (cfg1, cfg2b), a split where it pays
+    (cfg2a: 8 tiles x 4 parts)."""
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.configs import CONFIGS
+    p4 = algos.fused_plan(CONFIGS["cfg4"], "tc3xbf16")
+    assert (p4["block_m"], p4["block_n"], p4["m_tiles"], p4["ctas"]) == (256, 256, 98, 148)
+    for name in ("cfg1", "cfg2b"):
+        p = algos.fused_plan(CONFIGS[name], "tc3xbf16")
+        assert p["block_m"] == 128 and p["ctas"] == p["m_tiles"] * p["n_tiles"] == 25, (name, p)
+    p2a = algos.fused_plan(CONFIGS["cfg2a"], "tc3xbf16")
+    assert p2a["block_m"] == 128 and p2a["m_tiles"] * p2a["n_tiles"] == 8 and p2a["ctas"] == 32
