@@ -79,7 +79,8 @@ struct TmaParams {
 };
 
 constexpr int TRACE_SLOTS = 32;
-constexpr int MAX_TAIL_OTHERS = 3;  // tail tiles are split into at most 4 K parts
+constexpr int MAX_TAIL_OTHERS = 3;  // over-full grids: tail tiles split into at most 4 K parts
+constexpr int MAX_SHORT_PARTS = 16;  // short grids (tiles < clusters) with long reductions
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -464,34 +465,41 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                     ptx::tmem_ld_32x32b_x32(lane_tm + c0, r);
                     // every other part's values of the chunk in flight at once (one L2
                     // round trip per chunk), then the sum in part order
-                    float4 pv[MAX_TAIL_OTHERS + 1][8];  // indexed by part (own slot unused)
-#pragma unroll
-                    for (int q = 0; q <= MAX_TAIL_OTHERS; ++q) {
-                        if (q < P && q != it.part) {
-                            const float4* src = reinterpret_cast<const float4*>(
-                                                    slab_of + (int64_t)q * CG * slab) +
-                                                (int64_t)(ci * 8) * TMA_BM + row;
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) pv[q][j] = __ldcg(src + (int64_t)j * TMA_BM);
-                        }
-                    }
+                    // parts in groups of 4: every other part's values of a group in flight at
+                    // once (one L2 round trip per group), summed in part order
                     ptx::tmem_ld_wait();
                     float v[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0.f;
+#pragma unroll 1
+                    for (int q0 = 0; q0 < P; q0 += 4) {
+                        float4 pv[4][8];
 #pragma unroll
-                    for (int q = 0; q <= MAX_TAIL_OTHERS; ++q) {  // sum over parts in part order
-                        if (q >= P) break;
-                        if (q == it.part) {
+                        for (int o = 0; o < 4; ++o) {
+                            const int q = q0 + o;
+                            if (q < P && q != it.part) {
+                                const float4* src = reinterpret_cast<const float4*>(
+                                                        slab_of + (int64_t)q * CG * slab) +
+                                                    (int64_t)(ci * 8) * TMA_BM + row;
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
-                        } else {
+                                for (int j = 0; j < 8; ++j) pv[o][j] = __ldcg(src + (int64_t)j * TMA_BM);
+                            }
+                        }
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                v[4 * j] += pv[q][j].x;
-                                v[4 * j + 1] += pv[q][j].y;
-                                v[4 * j + 2] += pv[q][j].z;
-                                v[4 * j + 3] += pv[q][j].w;
+                        for (int o = 0; o < 4; ++o) {
+                            const int q = q0 + o;
+                            if (q >= P) break;
+                            if (q == it.part) {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    v[4 * j] += pv[o][j].x;
+                                    v[4 * j + 1] += pv[o][j].y;
+                                    v[4 * j + 2] += pv[o][j].z;
+                                    v[4 * j + 3] += pv[o][j].w;
+                                }
                             }
                         }
                     }
@@ -749,6 +757,24 @@ struct TmaPlan {
 // Cost model per candidate (cg, bn): waves over the persistent units times the per-tile
 // time, which is the slower of the MMA issue time and the operand bytes the CTA pulls at
 // the L2->SM rate the CG=1 kernel sustained under ncu (~40 B/cycle/SM).
+// K parts of each tail tile (1 = no split): parts <= units / tail so every part has its own
+// cluster (an owner spins on its parts); >= min K blocks per part; at most 4 on an over-full
+// grid, 16 on a short one; and only when the MMA time a split takes off a tile exceeds the
+// fixup's cost (park, publish, wait, sum: 2-3 us; cfg1 / cfg2b are faster unsplit).
+static int tail_split_parts(int64_t tiles, int units, int num_kb, int bn) {
+    const int64_t tail = tiles % units;
+    if (tail == 0) return 1;
+    const int min_kbp = tiles > units ? 4 : 2;
+    int parts = (int)std::min<int64_t>(std::min<int64_t>(units / tail, num_kb / min_kbp),
+                                       tiles > units ? MAX_TAIL_OTHERS + 1 : MAX_SHORT_PARTS);
+    const double tile_mma = 12.0 * num_kb * (bn / 2.0);  // cycles, as in plan_tma's model
+    if (parts >= 2 && tile_mma * (1.0 - 1.0 / parts) < 4000.0 && !std::getenv("CB_TMA_TAIL_ALWAYS"))
+        parts = 1;
+    if (parts < 2) return 1;
+    const int kbp = (num_kb + parts - 1) / parts;
+    return (num_kb + kbp - 1) / kbp;
+}
+
 static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     const int sms = sm_count();
     const char* force_cg = std::getenv("CB_TMA_CG");
@@ -769,11 +795,14 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
             const int n_tiles = (g.kpg + bn - 1) / bn;
             const int64_t tiles = m_tiles * n_tiles * g.G;
             const int units = sms / cg;
-            const double waves = std::ceil((double)tiles / units);
             const double mma = 12.0 * L.num_kb * (bn / 2.0);
             const double bytes = (double)L.num_kb * (2.0 * TMA_BM * 128 + 2.0 * (bn / cg) * 128);
             const double per_tile = std::max(mma, bytes / 40.0) + 2000.0;
-            const double cost = waves * per_tile;
+            // full waves, then the ragged tail cut into K parts (the fixup ~10k cycles with
+            // its pair / cluster overheads): huge reductions on few tiles fill the GPU
+            const int parts = tail_split_parts(tiles, units, L.num_kb, bn);
+            const double cost = (double)(tiles / units) * per_tile +
+                                (tiles % units ? per_tile / parts + (parts > 1 ? 10000.0 : 0.0) : 0.0);
             if (cost < best_cost * 0.97) {
                 best_cost = cost;
                 best.cg = cg;
@@ -812,14 +841,7 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     const char* no_tail = std::getenv("CB_TMA_TAIL");
     const int64_t tail = tiles % units;
     if (pl.splits == 1 && tail > 0 && !(no_tail && std::atoi(no_tail) == 0)) {
-        const int min_kbp = tiles > units ? 4 : 2;
-        int parts = (int)std::min<int64_t>(std::min<int64_t>(units / tail, L.num_kb / min_kbp),
-                                           MAX_TAIL_OTHERS + 1);
-        // the fixup (park, publish, wait, sum) costs ~2-3 us: split only when the MMA time it
-        // takes off a tail tile is larger (cfg1 / cfg2b: 9.7 -> 8.3 / 8.7 -> 6.3 us unsplit)
-        const double tile_mma = 12.0 * L.num_kb * (pl.bn / 2.0);  // cycles, as in the model
-        if (parts >= 2 && tile_mma * (1.0 - 1.0 / parts) < 4000.0 && !std::getenv("CB_TMA_TAIL_ALWAYS"))
-            parts = 1;
+        int parts = tail_split_parts(tiles, units, L.num_kb, pl.bn);
         if (parts >= 2) {
             pl.tail_kbp = (L.num_kb + parts - 1) / parts;
             parts = (L.num_kb + pl.tail_kbp - 1) / pl.tail_kbp;

@@ -174,7 +174,8 @@ def test_fused_tile_plans(lib):
     CTA pairs with a tail split on the big grid (cfg4: 98 pair tiles on 74 pairs, the 24 tail
     tiles in 3 K parts -> 74 + 72 items on 148 CTAs), single CTAs and no split on short grids
     whose tiles are too short for the fixup to pay (cfg1, cfg2b), a split where it pays
-    (cfg2a: 8 tiles x 4 parts)."""
+    (cfg2a: 8 tiles x 9 parts), and a huge reduction on few tiles cut into up to 16 K parts
+    with CTA pairs (C=2048 7x7 at 56x56: 13 pair tiles x 5 parts)."""
     from paper_2407_10730_b200 import algos
     from paper_2407_10730_b200.configs import CONFIGS
     p4 = algos.fused_plan(CONFIGS["cfg4"], "tc3xbf16")
@@ -183,4 +184,7 @@ def test_fused_tile_plans(lib):
         p = algos.fused_plan(CONFIGS[name], "tc3xbf16")
         assert p["block_m"] == 128 and p["ctas"] == p["m_tiles"] * p["n_tiles"] == 25, (name, p)
     p2a = algos.fused_plan(CONFIGS["cfg2a"], "tc3xbf16")
-    assert p2a["block_m"] == 128 and p2a["m_tiles"] * p2a["n_tiles"] == 8 and p2a["ctas"] == 32
+    assert p2a["block_m"] == 128 and p2a["m_tiles"] * p2a["n_tiles"] == 8 and p2a["ctas"] == 72
+    from paper_2407_10730_b200.descriptor import parse_key
+    big = algos.fused_plan(parse_key("n1_c2048x56x56_f256x7x7_s1x1_p3x3_d1x1_g1_b0"), "tc3xbf16")
+    assert (big["block_m"], big["m_tiles"], big["ctas"]) == (256, 13, 130), big

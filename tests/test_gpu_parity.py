@@ -345,3 +345,19 @@ def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
         assert fused_layout(d, "tc3xbf16")["path"] == 2, d
         inp, (x, w, b) = _inputs(d)
         _check_conv(d, conv_fused(inp, variant="tc3xbf16"), orc.conv_direct_naive(d, x, w, b))
+
+
+@pytest.mark.parametrize("variant", ["tc3xbf16", "tc3xtf32"])
+def test_short_grid_many_k_parts(cuda, variant):
+    """Few output tiles with a long reduction: each tile is cut into up to 16 K parts
+    (fixup sums the parts in groups of 4, in part order); deterministic and within tolerance."""
+    from paper_2407_10730_b200.algos import conv_fused, fused_plan
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    d = ConvDescriptor(batch=1, in_channels=1024, in_h=14, in_w=14, out_channels=64, k_h=3, k_w=3,
+                       pad_h=1, pad_w=1, has_bias=True)
+    plan = fused_plan(d, variant)
+    assert plan["ctas"] > 4 * plan["m_tiles"] * plan["n_tiles"], plan  # more than 4 parts a tile
+    inp, (x, w, b) = _inputs(d)
+    y1 = conv_fused(inp, variant=variant)
+    _check_conv(d, y1, orc.conv_im2col64(d, x, w, b))
+    assert np.array_equal(y1, conv_fused(inp, variant=variant))
