@@ -607,6 +607,28 @@ act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
     const int nq = cw / VEC;
     const int pw = min(32, HW - p0);
     const int64_t obase = (n * HW + p0) * (int64_t)c_alloc + c0;
+    if (BF16 && nq == 8) {
+        // one (pixel, 8-channel group) per thread, no division; paired bf16x2 conversions
+        const int pix = threadIdx.x >> 3, q = threadIdx.x & 7;
+        if (pix < pw) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float a = tile[q * 8 + 2 * e][pix], b = tile[q * 8 + 2 * e + 1][pix];
+                uint32_t hb;
+                asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hb) : "f"(b), "f"(a));
+                const float ra = a - __uint_as_float(hb << 16), rb = b - __uint_as_float(hb & 0xffff0000u);
+                uint32_t lb;
+                asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lb) : "f"(rb), "f"(ra));
+                h[e] = hb;
+                l[e] = lb;
+            }
+            const int64_t o = obase + (int64_t)pix * c_alloc + q * 8;
+            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(hi_out) + o) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(lo_out) + o) = make_uint4(l[0], l[1], l[2], l[3]);
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < 32 * nq; e += 256) {
         const int pix = e / nq, q = e - pix * nq;
         if (pix >= pw) break;
