@@ -627,6 +627,7 @@ act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
             *reinterpret_cast<uint4*>(static_cast<uint16_t*>(hi_out) + o) = make_uint4(h[0], h[1], h[2], h[3]);
             *reinterpret_cast<uint4*>(static_cast<uint16_t*>(lo_out) + o) = make_uint4(l[0], l[1], l[2], l[3]);
         }
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // the packing before us (K3) is complete
         return;
     }
     for (int e = threadIdx.x; e < 32 * nq; e += 256) {
@@ -637,6 +638,68 @@ act_split_nhwc_kernel(int C, int HW, int c_alloc, const float* __restrict__ x,
         for (int j = 0; j < VEC; ++j) v[j] = tile[q * VEC + j][pix];
         store_split16<BF16, VEC>(hi_out, lo_out, obase + (int64_t)pix * c_alloc + q * VEC, v);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the packing before us (K3) is complete
+}
+
+// K0, wide variant (bf16, HW % 4 == 0, 64-channel groups): a block splits 128 consecutive
+// pixels of the flattened (n, p) index x 64 channels -- float4 loads of 4-pixel groups (a
+// warp reads 512 contiguous bytes of a channel row), no partly empty pixel blocks.
+constexpr int AS_PX = 128;
+// tile[ch][px] with the 4-pixel groups of row ch XOR-swizzled by ch / 8: the float4 row
+// writes stay contiguous and the transposed reads (8 channel groups x 4 pixels per warp)
+// hit 32 distinct banks
+__device__ __forceinline__ int as_idx(int ch, int px) {
+    return ch * AS_PX + ((((px >> 2) ^ (ch >> 3)) & 31) << 2) + (px & 3);
+}
+__global__ void __launch_bounds__(256)
+act_split_wide_kernel(int C, int HW, int64_t npix, int c_alloc, const float* __restrict__ x,
+                      void* __restrict__ hi_out, void* __restrict__ lo_out, int* counters,
+                      int n_counters) {
+    __shared__ __align__(16) float tile[64 * AS_PX];
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = threadIdx.x; i < n_counters; i += 256) counters[i] = 0;
+    const int64_t j0 = (int64_t)blockIdx.x * AS_PX;
+    const int c0 = blockIdx.y * 64;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t jg = j0 + 4 * lane;
+    const bool gvalid = jg < npix;
+    const int64_t n = gvalid ? jg / HW : 0;
+    const float* xg = x + n * (int64_t)C * HW + (jg - n * HW);
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int c = c0 + warp + 8 * i;
+        v[i] = (gvalid && c < C) ? __ldg(reinterpret_cast<const float4*>(xg + (int64_t)c * HW))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<float4*>(tile + as_idx(warp + 8 * i, 4 * lane)) = v[i];
+    __syncthreads();
+    const int q = threadIdx.x & 7;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int pix = (threadIdx.x >> 3) + 32 * k;
+        if (j0 + pix >= npix) break;
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float a = tile[as_idx(q * 8 + 2 * e, pix)];
+            const float b = tile[as_idx(q * 8 + 2 * e + 1, pix)];
+            uint32_t hb;
+            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hb) : "f"(b), "f"(a));
+            const float ra = a - __uint_as_float(hb << 16), rb = b - __uint_as_float(hb & 0xffff0000u);
+            uint32_t lb;
+            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lb) : "f"(rb), "f"(ra));
+            h[e] = hb;
+            l[e] = lb;
+        }
+        const int64_t o = (j0 + pix) * (int64_t)c_alloc + c0 + q * 8;
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(hi_out) + o) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(lo_out) + o) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the packing before us (K3) is complete
 }
 
 // K0 for a folded layout (FusedLayout::fold): [N][H][Q][c_alloc] rows whose channel
@@ -671,6 +734,7 @@ act_fold_split_kernel(Geom g, int c_alloc, const float* __restrict__ x, void* __
         }
         store_split16<BF16, VEC>(hi_out, lo_out, pix * c_alloc + q * VEC, v);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the packing before us (K3) is complete
 }
 
 // K3 (fused layout): OIHW -> rows K x kw_pad, k = ((r*S + s)*chk + cb)*CB + ci, zero padded,
@@ -688,6 +752,9 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
                          void* __restrict__ lo_out, int fold, int stack_rs, int k_orig) {
     constexpr int VEC = BF16 ? 8 : 4;
     extern __shared__ float ws_tile[];  // [WS_CH][R*S]
+    // the activation split (K0) does not read the weights: it may start right away and
+    // waits for this grid only at its end (griddepcontrol.wait), before the conv reads both
+    asm volatile("griddepcontrol.launch_dependents;");
     const int f = blockIdx.y;
     const int c0 = blockIdx.x * WS_CH;
     const int RS = R * S;
@@ -737,6 +804,26 @@ weight_split_taps_kernel(int K, int cpg, int R, int S, int CB, int chk, int kw_p
     }
 }
 
+// K0 launches use programmatic stream serialization: they may start while the weight split
+// (K3) before them still runs (K3 triggers griddepcontrol.launch_dependents at its start; K0
+// waits for it at its end), so the pair costs one launch gap instead of a fork and a join.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, int block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    static const bool no_pdl = std::getenv("CB_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void* hi, void* lo,
                      int* counters, int n_counters, cudaStream_t st, int fold) {
     if (g.N == 0) return CB_OK;
@@ -747,23 +834,33 @@ int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void
         const int blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (runs + 255) / 256),
                                                   (int64_t)sm_count() * 16);
         if (bf16)
-            act_fold_split_kernel<true><<<blocks, 256, 0, st>>>(g, c_alloc, x, hi, lo, counters,
-                                                                 n_counters);
+            launch_pdl(act_fold_split_kernel<true>, dim3(blocks), 256, 0, st, g, c_alloc, x, hi, lo,
+                       counters, n_counters);
         else
-            act_fold_split_kernel<false><<<blocks, 256, 0, st>>>(g, c_alloc, x, hi, lo, counters,
-                                                                  n_counters);
+            launch_pdl(act_fold_split_kernel<false>, dim3(blocks), 256, 0, st, g, c_alloc, x, hi, lo,
+                       counters, n_counters);
         return check_launch("act_fold_split");
+    }
+    const int64_t in_pix = (int64_t)g.N * g.HW;  // input pixels (not the conv's output npix)
+    if (bf16 && g.HW % 4 == 0 && c_alloc % 64 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        !std::getenv("CB_K0_NARROW") && (in_pix + AS_PX - 1) / AS_PX <= 0x7fffffffLL) {
+        if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
+            return fail(CB_ERR_MISALIGNED, "activation workspace must be 16-byte aligned");
+        const dim3 wgrid((unsigned)((in_pix + AS_PX - 1) / AS_PX), (unsigned)(c_alloc / 64));
+        launch_pdl(act_split_wide_kernel, wgrid, 256, 0, st, g.C, g.HW, in_pix, c_alloc, x, hi, lo,
+                   counters, n_counters);
+        return check_launch("act_split_wide");
     }
     dim3 grid((unsigned)((g.HW + 31) / 32), (unsigned)((c_alloc + 63) / 64), (unsigned)g.N);
     if (grid.z > 65535) return fail(CB_ERR_UNSUPPORTED, "batch too large for act_split grid");
     if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
         return fail(CB_ERR_MISALIGNED, "activation workspace must be 16-byte aligned");
     if (bf16)
-        act_split_nhwc_kernel<true><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo,
-                                                           counters, n_counters);
+        launch_pdl(act_split_nhwc_kernel<true>, grid, 256, 0, st, g.C, g.HW, c_alloc, x, hi, lo,
+                   counters, n_counters);
     else
-        act_split_nhwc_kernel<false><<<grid, 256, 0, st>>>(g.C, g.HW, c_alloc, x, hi, lo,
-                                                            counters, n_counters);
+        launch_pdl(act_split_nhwc_kernel<false>, grid, 256, 0, st, g.C, g.HW, c_alloc, x, hi, lo,
+                   counters, n_counters);
     return check_launch("act_split_nhwc");
 }
 
