@@ -292,14 +292,16 @@ static bool band_plan(const Geom& g, int max_rows, int64_t units, BandPlan* bp, 
     // at least ~2 waves of blocks: shrink the channel group, then the band (>= 256 px)
     static const int waves = [] {
         const char* e = getenv("CB_BAND_WAVES");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 2;  // with the TMA-staged window: cfg4 K1 59 -> 50 us (0: off)
     }();
     const int64_t want = (int64_t)waves * sm_count() * 8;
     auto blocks = [&](int t, int c) {
         return units * ((max_rows + t - 1) / t) * ((g.C + c - 1) / c);
     };
     while (blocks(tr, cc) < want && cc > 1) cc = (cc + 1) / 2;
-    while (blocks(tr, cc) < want && tr > 1 && (tr / 2) * g.Q >= 256) tr /= 2;
+    // (bands are not shrunk by default: smaller bands measured slower -- cfg2b 8.4 -> 10.5 us)
+    static const bool shrink_bands = getenv("CB_BAND_SHRINK_ROWS") != nullptr;
+    while (shrink_bands && blocks(tr, cc) < want && tr > 1 && (tr / 2) * g.Q >= 256) tr /= 2;
     bp->TR = tr;
     bp->IR = (tr - 1) * g.sh + (g.R - 1) * g.dh + 1;
     bp->IWp = g.W + 2 * g.pw;
