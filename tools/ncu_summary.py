@@ -33,7 +33,7 @@ KEYS = [
 ]
 
 
-SHORT = {"conv_tma_kernel": "conv_tma", "act_split_nhwc_kernel": "act_split",
+SHORT = {"conv_tma_kernel": "conv_tma", "act_split_nhwc_kernel": "act_split", "act_split_wide_kernel": "act_split",
          "act_fold_split_kernel": "act_fold_split", "weight_split_taps_kernel": "weight_split_taps",
          "im2col_band_kernel": "im2col_band", "im2col_kernel": "im2col_kernel",
          "conv_tc_kernel": "conv_tc", "conv_ts_kernel": "conv_ts", "gemm_ts_kernel": "gemm_ts",
