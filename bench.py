@@ -393,7 +393,10 @@ def run_ours(args):
 
 
 def breakdown(d, fused_variant, runs: int = 5):
-    """Per-phase CUDA-event times (us, mean of `runs`) of the three GPU algorithms."""
+    """Per-phase CUDA-event times (us, mean of `runs`) of the three GPU algorithms.  Each
+    algorithm is captured once into a CUDA graph with external phase events and replayed
+    (the harness's graph mode), so a phase's time is its kernels', not the host's launch
+    latency between an eager event and the kernel after it."""
     import torch
     from paper_2407_10730_b200 import algos
     from paper_2407_10730_b200.harness import RunConfig, make_inputs, to_device
@@ -403,13 +406,19 @@ def breakdown(d, fused_variant, runs: int = 5):
     for name, fn in (("im2col_gemm", lambda i, l: algos.conv_baseline_im2col_gemm(i, l)),
                      ("sconv", lambda i, l: algos.conv_main_blocked_direct(i, l)),
                      ("fused", lambda i, l: algos.conv_fused(i, l, variant=fused_variant))):
-        led = EventLedger()
+        fn(inp, EventLedger())  # eager first call: plans, kernel attributes, tensor maps
+        led = EventLedger(external=True)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            fn(inp, led)
         reps = []
         for r in range(runs + 2):
-            led.reset()
-            fn(inp, led)
+            graph.replay()
             if r >= 2:
                 reps.append(led.snapshot())
+        del graph
         st = aggregate(reps)
         op = st.operation_ns_mean
         pack = st.phase_ns_mean[Phase.IN_PACKING] + (st.phase_ns_mean[Phase.PRE_REORDER]
@@ -419,7 +428,8 @@ def breakdown(d, fused_variant, runs: int = 5):
                      "pack_share": pack / op if op else None,
                      "phases_us": {p.name.lower(): st.phase_ns_mean[p] / 1e3 for p in Phase
                                    if st.calls[p]},
-                     "calls": {p.name.lower(): st.calls[p] for p in Phase if st.calls[p]}}
+                     "calls": {p.name.lower(): st.calls[p] for p in Phase if st.calls[p]},
+                     "timing": "CUDA graph replay, external phase events"}
     torch.cuda.synchronize()
     return out
 
