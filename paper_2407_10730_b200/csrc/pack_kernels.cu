@@ -383,11 +383,10 @@ int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, i
 template <bool BF16>
 __global__ void weight_split_kernel(int rows, int kdim, int kdim_pad, const float* __restrict__ w,
                                     void* __restrict__ hi_out, void* __restrict__ lo_out) {
-    const int64_t total = (int64_t)rows * kdim_pad;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / kdim_pad);
-        const int k = (int)(i - (int64_t)r * kdim_pad);
+    // rows by blockIdx.y, columns by a block-stride loop: no 64-bit division per element
+    for (int r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kdim_pad; k += gridDim.x * blockDim.x) {
+        const int64_t i = (int64_t)r * kdim_pad + k;
         const float v = k < kdim ? w[(int64_t)r * kdim + k] : 0.f;
         if (BF16) {
             const uint16_t h = bf16_rn_bits(v);
@@ -465,7 +464,7 @@ int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float
                         void* lo, cudaStream_t st) {
     const int64_t total = (int64_t)rows * kdim_pad;
     if (total == 0) return CB_OK;
-    const int grid = grid_for(total, 256);
+    const dim3 grid((unsigned)std::min<int64_t>((kdim_pad + 255) / 256, 16), (unsigned)std::min(rows, 65535));
     if (bf16)
         weight_split_kernel<true><<<grid, 256, 0, st>>>(rows, kdim, kdim_pad, w, hi, lo);
     else
