@@ -124,6 +124,9 @@ int tma_tail_counters(const Geom& g, const FusedLayout& L);
 int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
                    const float* bias, float* y, cudaStream_t st);
 int ts_plan_query(const Geom& g, cb_tile_plan* out);
+int ts_weight_kdim(const Geom& g, int* pair, int* pf);
+int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, const float* w, void* hi, void* lo,
+                              cudaStream_t st);
 int ffma_plan_query(const Geom& g, int64_t npix, bool allow_split, cb_tile_plan* out);
 int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
               const void* w_lo, const float* bias, float* out, int add_mode, int zero_kind,
@@ -493,7 +496,9 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
     out->chunk_channels = L.tma ? L.cb : 0;
     out->chunk_bytes = L.tma ? L.chunk_bytes : 0;
     out->k_blocks = L.tma ? L.num_kb : (g.kdim + 128 / L.eb - 1) / (128 / L.eb);
-    out->weight_cols = L.tma ? L.kw_pad : cb_split_kdim(g.kdim);  // K7 / K4: plain split rows
+    int ts_pair = 0, ts_pf = 0;
+    out->weight_cols = L.tma ? L.kw_pad
+                             : cb_split_kdim(L.ts ? ts_weight_kdim(g, &ts_pair, &ts_pf) : g.kdim);  // K7 / K4
     out->workspace_bytes = act_ws_bytes(gk, L);
     return CB_OK;
 }
@@ -524,6 +529,11 @@ int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, vo
         return launch_weight_split_taps(bf16, gk, L.cb, L.chk, L.kw_pad, w, w_hi, w_lo,
                                         (cudaStream_t)stream, L.fold,
                                         L.stack == 1 ? g.RS : L.stack == 2 ? g.S : 0, g.K);
+    if (L.ts) {  // K7: plain split rows, or the pair layout with one pad tap per (c, r) row
+        int pair = 0, pf = 0;
+        const int kd = ts_weight_kdim(g, &pair, &pf);
+        if (pair) return launch_weight_split_pairs(g, pf, cb_split_kdim(kd), w, w_hi, w_lo, (cudaStream_t)stream);
+    }
     return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
                                (cudaStream_t)stream);
 }

@@ -57,6 +57,12 @@ struct TsParams {
     int tma_store;          // 1: epilogue stages 32-channel chunks in smem, TMA stores them
     float inv_q;            // 1 / Q (pixel -> output row without an integer division)
     int fixed;              // CB_TS_FIXED_LIST id of a compile-time producer, 0: generic
+    // pair mode (fixed producers, even horizontal stride, odd S): the reduction is laid out
+    // k = (c*R + r)*(S+1) + s' with one zero-weight pad tap per (c, r) row -- at s' = 0 when
+    // pf = 1, at s' = S otherwise -- so each k pair (s', s'+1) is one 8-byte aligned LDS.64
+    // of two adjacent window columns (the A build is bound by the LDS instruction rate)
+    int pair;
+    int pf;
     unsigned long long* trace;  // diagnostics (CB_TS_TRACE): clock64 stamps of CTAs 0..3
 };
 
@@ -182,6 +188,54 @@ __device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint3
     }
 }
 
+// Pair-mode producer: groups [G0, G1) of 8 elements of the padded layout (S' = S + 1 taps a
+// row, even), each pair one LDS.64 at xs_pair + row offset + 8 * (s' / 2).
+template <int C, int R, int S, int G0, int G1>
+__device__ __forceinline__ void build_pairs(uint32_t xs_pair, uint32_t cstride, uint32_t rstride,
+                                            uint32_t a_hi, uint32_t a_lo) {
+    constexpr int SP = S + 1, KD = C * R * SP, NG = G1 - G0, D = 3;
+    float2 v[D + 1][4];
+#pragma unroll
+    for (int step = 0; step < NG + D; ++step) {
+        if (step < NG) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = (G0 + step) * 8 + 2 * e;
+                if (k < KD) {
+                    const int cr = k / SP, sp = k % SP;
+                    const uint32_t a = xs_pair + (cr / R) * cstride + (cr % R) * rstride + 4 * sp;
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+                                 : "=f"(v[step % (D + 1)][e].x), "=f"(v[step % (D + 1)][e].y)
+                                 : "r"(a));
+                } else {
+                    v[step % (D + 1)][e] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+        if (step >= D) {
+            const int gi = step - D;
+            uint32_t hv[4], lv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) split_pair(v[gi % (D + 1)][e].x, v[gi % (D + 1)][e].y, hv[e], lv[e]);
+            ptx::tmem_st_32x32b_x4(a_hi + (G0 + gi) * 4, hv);
+            ptx::tmem_st_32x32b_x4(a_lo + (G0 + gi) * 4, lv);
+        }
+    }
+}
+
+template <int C, int R, int S>
+__device__ __forceinline__ void build_pairs_part(int kpart, uint32_t xs_pair, uint32_t cstride,
+                                                 uint32_t rstride, uint32_t a_hi, uint32_t a_lo) {
+    constexpr int G = (C * R * (S + 1) + 7) / 8;
+    constexpr int G1 = (G + 2) / 3, G2 = G1 + (G - G1 + 1) / 2;
+    if (kpart == 0)
+        build_pairs<C, R, S, 0, G1>(xs_pair, cstride, rstride, a_hi, a_lo);
+    else if (kpart == 1)
+        build_pairs<C, R, S, G1, G2>(xs_pair, cstride, rstride, a_hi, a_lo);
+    else
+        build_pairs<C, R, S, G2, G>(xs_pair, cstride, rstride, a_hi, a_lo);
+}
+
 // the three producer warps of a lane quadrant take contiguous thirds of the 8-element groups
 template <int C, int R, int S>
 __device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_t cstride,
@@ -301,18 +355,30 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             if (p.fixed && !(p.debug & 16)) {
                 if (i < 2) {  // columns past the written groups: zero once per A buffer
                     const uint32_t z[4] = {0u, 0u, 0u, 0u};
-                    for (int c4 = ((g.kdim + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
+                    const int kd = p.pair ? g.C * g.R * (g.S + 1) : g.kdim;
+                    for (int c4 = ((kd + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
                         ptx::tmem_st_32x32b_x4(a_hi + c4, z);
                         ptx::tmem_st_32x32b_x4(a_lo + c4, z);
                     }
                 }
                 const uint32_t cstride = 4u * p.box_rows * p.box_w, rstride = 4u * g.dh * p.box_w;
-                switch (p.fixed) {
+                if (p.pair) {
+                    const uint32_t xs_pair = xs - 4u * p.pf;  // 8-byte aligned (plan_ts)
+                    switch (p.fixed) {
+#define CB_TS_CASE(id, c, r, s) \
+    case id: if (s % 2) build_pairs_part<c, r, s>(kpart, xs_pair, cstride, rstride, a_hi, a_lo); break;
+                        CB_TS_FIXED_LIST(CB_TS_CASE)
+#undef CB_TS_CASE
+                        default: break;
+                    }
+                } else {
+                    switch (p.fixed) {
 #define CB_TS_CASE(id, c, r, s) \
     case id: build_fixed_part<c, r, s>(kpart, xs, cstride, rstride, a_hi, a_lo, swap); break;
-                    CB_TS_FIXED_LIST(CB_TS_CASE)
+                        CB_TS_FIXED_LIST(CB_TS_CASE)
 #undef CB_TS_CASE
-                    default: break;
+                        default: break;
+                    }
                 }
             }
             for (int kc = kpart; kc < nchunks && !p.fixed && !(p.debug & 16); kc += KPARTS) {
@@ -497,7 +563,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
 // ----------------------------------------------------------------------------------------
 struct TsPlan {
     bool ok;
-    int kp, n_pad, kb_w, box_rows, box_w, x0;
+    int kp, n_pad, kb_w, box_rows, box_w, x0, pair, pf, kdim;
     uint32_t stage_bytes, stage_stride, w_half_bytes;
     int nwin;
     bool tma_store;
@@ -518,12 +584,24 @@ static TsPlan plan_ts(const Geom& g) {
     if (g.G != 1 || g.npix == 0) return pl;
     // int32 tile walk and the float pixel -> row division (TileWalk, div_q)
     if (g.PQ >= (1 << 21) || (int64_t)g.N * ((g.PQ + TS_BM - 1) / TS_BM) >= (1LL << 31) - 1024) return pl;
-    pl.kp = round_up(g.kdim, 32);
     pl.n_pad = round_up(g.K, 16);
-    pl.kb_w = round_up(g.kdim, 64);  // == cb_split_kdim(kdim)
-    if (pl.n_pad > 256 || 2 * pl.n_pad + 2 * pl.kp > TS_TMEM_COLS) return pl;
     pl.x0 = round_up(g.pw, 4);  // 16-byte aligned window start
-    pl.box_w = round_up(g.W + g.pw + pl.x0, 4);
+    // pair mode: compile-time producer, even horizontal stride, odd S, the padded reduction
+    // fits TMEM next to two accumulators
+    pl.pair = 0;
+    pl.pf = (pl.x0 - g.pw) & 1;
+    const int kd_pair = g.C * g.R * (g.S + 1);
+    static const bool no_pair = std::getenv("CB_TS_NO_PAIR") != nullptr;
+    if (!no_pair && ts_fixed_id(g) && g.S % 2 == 1 && g.sw % 2 == 0 &&
+        2 * pl.n_pad + 2 * round_up(kd_pair, 32) <= TS_TMEM_COLS)
+        pl.pair = 1;
+    pl.kdim = pl.pair ? kd_pair : g.kdim;
+    pl.kp = round_up(pl.kdim, 32);
+    pl.kb_w = round_up(pl.kdim, 64);  // == cb_split_kdim(kdim)
+    if (pl.n_pad > 256 || 2 * pl.n_pad + 2 * pl.kp > TS_TMEM_COLS) return pl;
+    // window columns: every tap of every output column (+ the pad tap past the last one)
+    const int need = (g.Q - 1) * g.sw + (pl.x0 - g.pw) + (g.S - 1) * g.dw + 1 + (pl.pair && !pl.pf ? 1 : 0);
+    pl.box_w = round_up(std::max(g.W + g.pw + pl.x0, need), 4);
     const int out_rows = std::min(g.P, (TS_BM - 1) / std::max(1, g.Q) + 2);
     pl.box_rows = (out_rows - 1) * g.sh + (g.R - 1) * g.dh + 1;
     if (pl.box_w > 256 || pl.box_rows > 256 || g.C > 256 || (g.W % 4) != 0) return pl;
@@ -550,6 +628,15 @@ static TsPlan plan_ts(const Geom& g) {
 
 // Used by fused_layout: the direct kernel serves this descriptor (bf16 split only).
 bool ts_eligible(const Geom& g) { return plan_ts(g).ok; }
+
+// The K7 weight layout: reduction length of the packed rows (C*R*(S+1) in pair mode) and,
+// in pair mode, the pad position (*pf = 1: pad tap first in each (c, r) row).
+int ts_weight_kdim(const Geom& g, int* pair, int* pf) {
+    const TsPlan pl = plan_ts(g);
+    *pair = pl.pair;
+    *pf = pl.pf;
+    return pl.pair ? pl.kdim : g.kdim;
+}
 
 int ts_plan_query(const Geom& g, cb_tile_plan* out) {
     const TsPlan pl = plan_ts(g);
@@ -642,6 +729,8 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.tiles_per_img = (g.PQ + TS_BM - 1) / TS_BM;
     prm.inv_q = 1.0f / (float)g.Q;
     prm.fixed = ts_fixed_id(g);
+    prm.pair = pl.pair;
+    prm.pf = pl.pf;
     prm.total_tiles = (int64_t)g.N * prm.tiles_per_img;
     prm.box_rows = pl.box_rows;
     prm.box_w = pl.box_w;

@@ -62,7 +62,15 @@ __device__ __forceinline__ uint32_t probe_build(uint32_t xs, uint32_t cstride, u
 #pragma unroll
     for (int gi = 0; gi < 19; ++gi) {
         float v[8];
-        if (MODE != 2) {
+        if (MODE == 4) {  // LDS.64 pairs (aligned): half the load instructions, same bytes
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+                float2 t;
+                const uint32_t ad = (xs & ~7u) + 8u * (uint32_t)((gi * 8 + e) % 56);
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(t.x), "=f"(t.y) : "r"(ad));
+                v[e] = t.x; v[e + 1] = t.y;
+            }
+        } else if (MODE != 2) {
 #pragma unroll
             for (int e = 0; e < 8; e += 2) load_pair<3, 7, 7>(gi * 8 + e, xs, xa, xb, cstride, rstride, swap, v[e], v[e + 1]);
         } else {
@@ -70,7 +78,7 @@ __device__ __forceinline__ uint32_t probe_build(uint32_t xs, uint32_t cstride, u
             for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(acc + e);
         }
         uint32_t hv[4], lv[4];
-        if (MODE == 3) {
+        if (MODE == 3 || MODE == 4) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc ^= __float_as_uint(v[e]);
             continue;
@@ -128,7 +136,7 @@ void run_mode(unsigned long long* d) {
     k<<<148, 128, 160 * 1024>>>(d, iters);
     unsigned long long h;
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    const char* names[] = {"load+split+store", "load+split", "store only", "load only"};
+    const char* names[] = {"load+split+store", "load+split", "store only", "load only", "LDS.64 only"};
     printf("4 warps %-18s cycles per tile %.0f  %s\n", names[MODE], (double)h / 148 / iters,
            cudaGetErrorString(cudaGetLastError()));
 }
@@ -153,6 +161,6 @@ int main() {
     run<4, true>(d);
     run<8, true>(d);
     run<12, true>(d);
-    run_mode<0>(d); run_mode<1>(d); run_mode<2>(d); run_mode<3>(d);
+    run_mode<0>(d); run_mode<1>(d); run_mode<2>(d); run_mode<3>(d); run_mode<4>(d);
     return 0;
 }
