@@ -329,12 +329,15 @@ K7_SHAPES = [(3, 7, 7), (3, 3, 3), (3, 5, 5), (4, 3, 3), (4, 7, 7), (2, 5, 3), (
 
 @pytest.mark.parametrize("crs", K7_SHAPES)
 @pytest.mark.parametrize("stride", [1, 2])
-@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("generic", [False, True, "no_pair"])
 def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
     from paper_2407_10730_b200.algos import conv_fused, fused_layout
     from paper_2407_10730_b200.descriptor import ConvDescriptor
     c, r, s = crs
-    if generic:
+    if generic == "no_pair":  # compile-time producers without the padded pair layout
+        monkeypatch.setenv("CB_TS_NO_PAIR", "1")
+        generic = False
+    elif generic:
         monkeypatch.setenv("CB_TS_GENERIC", "1")
     for d in (ConvDescriptor(batch=2, in_channels=c, in_h=37, in_w=44, out_channels=24, k_h=r, k_w=s,
                              stride_h=stride, stride_w=stride, pad_h=r // 2, pad_w=s // 2, has_bias=True),
@@ -361,3 +364,17 @@ def test_short_grid_many_k_parts(cuda, variant):
     y1 = conv_fused(inp, variant=variant)
     _check_conv(d, y1, orc.conv_im2col64(d, x, w, b))
     assert np.array_equal(y1, conv_fused(inp, variant=variant))
+
+
+def test_activation_split_variants_agree(cuda, monkeypatch):
+    """K0's wide (flattened pixels, float4 loads, swizzled tile) and narrow variants write the
+    same split halves: the fused conv's result is bitwise the same with either."""
+    from paper_2407_10730_b200.algos import conv_fused
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    d = ConvDescriptor(batch=3, in_channels=96, in_h=10, in_w=14, out_channels=40, k_h=3, k_w=3,
+                       pad_h=1, pad_w=1, has_bias=True)
+    inp, (x, w, b) = _inputs(d)
+    y_wide = conv_fused(inp, variant="tc3xbf16")
+    _check_conv(d, y_wide, orc.conv_direct_naive(d, x, w, b))
+    monkeypatch.setenv("CB_K0_NARROW", "1")
+    assert np.array_equal(conv_fused(inp, variant="tc3xbf16"), y_wide)
