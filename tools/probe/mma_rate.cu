@@ -19,11 +19,15 @@ __global__ void __launch_bounds__(192, 1) mma_rate(unsigned long long* out) {
     uint8_t* a_s = smem;             // 128 x 128 B
     uint8_t* b_s = smem + 16384;     // N x 128 B
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 16384 + 256 * 128);
-    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
     volatile uint32_t* done = slot + 1;
     for (int i = threadIdx.x; i < (16384 + N * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
     const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) { ptx::mbar_init(bar, 1); *done = 0; ptx::fence_mbar_init(); }
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(bar, 1); ptx::mbar_init(bar + 2, 1); ptx::mbar_init(bar + 3, 1);
+        ptx::mbar_arrive(bar + 3);  // phase 0 complete: waits on it return at once
+        *done = 0; ptx::fence_mbar_init();
+    }
     ptx::fence_proxy_async_smem();
     if (warp == 5) ptx::tmem_alloc(slot, 512);
     ptx::tc_fence_before();
@@ -43,6 +47,12 @@ __global__ void __launch_bounds__(192, 1) mma_rate(unsigned long long* out) {
                 const uint64_t off = (uint64_t)((j & 3) * 2);
                 if (TS) ptx::umma_ts_bf16(tm, a_tm + (j & 3) * 8, db + off, idesc, j > 0);
                 else ptx::umma<true>(tm, da + off, db + off, idesc, j > 0);
+                if (SIDE == 5 && j % 6 == 5) ptx::umma_commit(bar + 2);  // K8: a commit per chunk
+                if (SIDE == 6 && j % 6 == 5) {  // + K8's per-chunk wait on a ready barrier and fence
+                    ptx::umma_commit(bar + 2);
+                    ptx::mbar_wait(bar + 3, 0);
+                    ptx::tc_fence_after();
+                }
             }
             ptx::umma_commit(bar);
         }
@@ -100,7 +110,7 @@ void run(unsigned long long* d) {
     const double cyc = (double)h[1] / 148 / ITER;
     const double side_bytes = SIDE ? (double)h[2] * 16384.0 / (double)h[1] : 0;  // per SM per cycle
     printf("%s N=%3d side=%s  cycles/MMA %.1f  (block0 %.1f)  floor %d  side B/cyc %.1f  %s\n", TS ? "TS" : "SS", N,
-           SIDE == 0 ? "none" : SIDE == 1 ? "ld  " : SIDE == 2 ? "st  " : SIDE == 3 ? "LDS " : "STS ", cyc, (double)h[0] / ITER, 128 * N / 256, side_bytes,
+           SIDE == 0 ? "none" : SIDE == 1 ? "ld  " : SIDE == 2 ? "st  " : SIDE == 3 ? "LDS " : SIDE == 4 ? "STS " : SIDE == 5 ? "cmt " : "fnc ", cyc, (double)h[0] / ITER, 128 * N / 256, side_bytes,
            e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
@@ -114,5 +124,6 @@ int main() {
     run<1, 128, 1>(d); run<1, 128, 2>(d);
     run<0, 64, 1>(d); run<0, 64, 2>(d);
     run<1, 64, 3>(d); run<1, 64, 4>(d); run<1, 128, 3>(d); run<0, 64, 3>(d);
+    run<1, 256, 5>(d); run<1, 64, 5>(d); run<1, 256, 6>(d); run<1, 64, 6>(d);
     return 0;
 }
