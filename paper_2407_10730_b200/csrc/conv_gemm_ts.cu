@@ -202,12 +202,15 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 if (BF16) {
                     uint32_t hv[16], lv[16];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const uint16_t h0 = bf16_rn_bits(v[2 * e]), h1 = bf16_rn_bits(v[2 * e + 1]);
-                        const uint16_t l0 = bf16_rn_bits(v[2 * e] - bf16_bits_to_f32(h0));
-                        const uint16_t l1 = bf16_rn_bits(v[2 * e + 1] - bf16_bits_to_f32(h1));
-                        hv[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-                        lv[e] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+                    for (int e = 0; e < 16; ++e) {  // paired conversions (2 values per cvt)
+                        const float a0 = v[2 * e], a1 = v[2 * e + 1];
+                        uint32_t h;
+                        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(a1), "f"(a0));
+                        const float r0 = a0 - __uint_as_float(h << 16), r1 = a1 - __uint_as_float(h & 0xffff0000u);
+                        uint32_t l;
+                        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(r1), "f"(r0));
+                        hv[e] = h;
+                        lv[e] = l;
                     }
                     ptx::tmem_st_32x32b_x16(a_hi, hv);
                     ptx::tmem_st_32x32b_x16(a_lo, lv);
