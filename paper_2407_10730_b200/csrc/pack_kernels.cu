@@ -526,8 +526,18 @@ unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int6
         const int n4 = np >> 2;
         const float4* s4 = reinterpret_cast<const float4*>(src);
         float4* d4 = reinterpret_cast<float4*>(dst);
-        // 4 vectors in flight per lane (the loop was latency-bound at one)
+        // 8 vectors in flight per lane (the loop was latency-bound at one)
         int i = lane;
+        for (; i + 224 < n4; i += 256) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(s4 + i + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                v[u].x += b; v[u].y += b; v[u].z += b; v[u].w += b;
+                d4[i + 32 * u] = v[u];
+            }
+        }
         for (; i + 96 < n4; i += 128) {
             float4 v[4];
 #pragma unroll
