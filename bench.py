@@ -2,7 +2,8 @@
 """bench.py -- the B200 conv path on BASELINE.json's headline workload (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--variant tc3xbf16|tc3xtf32|ffma] [--config cfg4] [--scaling weak|strong]
+                    [--variant auto|tc3xbf16|tc3xtf32|ffma] [--config cfg4]
+                    [--scaling strong|weak] [--dry-run]
 
 A step is one pass of the path over one batch: the fused implicit-GEMM conv of config 4
 (N=128, C=256, 14x14, K=256, 3x3, stride 1, pad 1): K3 weight split
@@ -10,24 +11,43 @@ A step is one pass of the path over one batch: the fused implicit-GEMM conv of c
 three every step.  Data is seeded synthetic U(-1,1) exactly as the reference's
 make_inputs draws it.
 
-* value        device-resident throughput, GFLOP/s summed over ranks: one FusedConv plan,
-               one CUDA graph per ring of 4 whole steps (a remainder of K replays per-step
-               graphs); 4 rotating input /
-               output sets (x 25.7 MB + y 25.7 MB each, plus the 44.6 MB workspace the
-               step rewrites: > 2x the 126 MB L2 over a ring cycle).  Time = max over ranks
-               of the CUDA-event time of exactly K steps between barrier + synchronize.
-* e2e          same metric through the same call with pinned HOST buffers: every step
-               copies x and w host->device and y device->host inside the timed region.
-* roofline     dominant kernel (conv_tma_kernel): algorithmic FLOPs / its mean launch
-               time (EventLedger IN_MICROKERNEL), vs the measured dense bf16 peak.
-* cpu_baseline the reference's own CPU algorithm (oracle/reference_port.py, a restatement
-               of algos.py) on a bounded sample of the same workload, rank 0 at N=1 only.
-* breakdown    per-step (phase) CUDA-event times of the three GPU algorithms on the
-               workload: Im2col-GEMM, SConv (blocked direct) and fused.
+Ranks: `--gpus N` starts N ranks itself (one per GPU, torch.distributed.run on 127.0.0.1;
+paper_2407_10730_b200/launch.py); under torchrun WORLD_SIZE must equal N.  Scaling is
+strong by default, as north_star specifies for configs 3 and 4: the global batch (128) is
+split into contiguous per-rank slices (shard.batch_shard), weights replicated, no
+collective on the data path -- NCCL carries only the barrier, the max-over-ranks time and
+the FLOP sum.  --scaling weak gives every rank the whole batch.
 
---impl reference: rank 0 times the reference CPU algorithm (port) with all host threads
-on the same config/metric and prints the same JSON line with "impl": "reference"; other
-ranks exit 0 without work.
+Keys of the JSON line (rank 0):
+* value        device-resident throughput, GFLOP/s over all ranks: one FusedConv plan per
+               rank, one CUDA graph per ring of 4 whole steps; 4 rotating input/output sets
+               plus the rewritten workspace (> 2x the 126 MB L2 per ring cycle at N=1).
+               Time = max over ranks of the CUDA-event time of exactly K steps between
+               barrier + synchronize.
+* e2e          the same metric through the package's host-buffer API (HostPipeline: x, w
+               host->device and y device->host inside the timed region every step);
+               e2e_dropin: the reference-facing drop-in conv_fused(numpy in -> numpy out),
+               per call, with and without the identity-keyed input cache.
+* roofline     dominant kernel (K6): algorithmic FLOPs / its mean launch time (CUDA events
+               captured between the step's kernels), against the split variant's
+               attainable peak (dense bf16 / 3 for 3xBF16, / 6 for 3xTF32); the fraction of
+               dense bf16 is a secondary field.
+* variants     the same workload with the north_star's 3xTF32 split (and 3xBF16).
+* configs      configs 1-4 x {fused, Im2col-GEMM, SConv}: graph-replayed phase times with an
+               L2 flush before every replay, GFLOP/s, roofline fractions of the fused kernel
+               and of the packing kernels (K1 / K2 GB/s vs the HBM peak).
+* cpu_baseline the reference CPU algorithms (the unmodified reference from baseline/_ref,
+               else the oracle port), rank 0 at N=1: 1 thread and all threads, both
+               algorithms, configs 1-4 on bounded samples; the headline value is SConv
+               (blocked direct) on cfg4, all threads.
+* parity       the reference CPU outputs of those samples against the GPU outputs of the
+               same images, including the timed graph's own output:
+               max|y - y_ref| / sqrt(C*R*S) <= 1e-4.
+
+--impl reference: rank 0 times the reference CPU algorithm with all host threads on the
+same config/metric and prints the same JSON line with "impl": "reference"; other ranks
+exit 0 without work.  --dry-run: the multi-rank control path (launcher, gloo barrier,
+max-over-ranks, sharding) without a GPU; the line says "dry_run": true.
 """
 
 from __future__ import annotations
@@ -51,9 +71,12 @@ METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"] \
     "conv GFLOP/s (2*N*K*P*Q*C*R*S/t) + pack/compute breakdown; % of roofline"
 UNIT = "GFLOP/s"
 RING = 4
+TOL = 1e-4
+TABLE_CONFIGS = ("cfg1", "cfg2a", "cfg2b", "cfg3", "cfg4")
+CPU_SAMPLE_IMAGES = 2
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -61,31 +84,30 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--variant", default=None)
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
-    ap.add_argument("--no-breakdown", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
+    ap.add_argument("--no-breakdown", action="store_true", help="skip the per-config table")
+    ap.add_argument("--no-variants", action="store_true", help="skip the 3xTF32 / 3xBF16 lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
-
-
-def dist_env():
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    return rank, world, local
+    ap.add_argument("--dry-run", action="store_true")
+    return ap.parse_args(argv)
 
 
 def workload(cfg_name: str, world: int, scaling: str, rank: int):
+    """(this rank's descriptor, first image of its slice in the global batch)."""
     from paper_2407_10730_b200.configs import CONFIGS
+    from paper_2407_10730_b200.shard import batch_shard
     d = CONFIGS[cfg_name]
     if scaling == "strong" and world > 1:
-        per = d.batch // world + (1 if rank < d.batch % world else 0)
-        d = replace(d, batch=max(1, per))
-    return d
+        start, count = batch_shard(d.batch, world, rank)
+        if count == 0:
+            raise SystemExit(f"rank {rank}: no images of {cfg_name} (batch {d.batch} < {world} ranks)")
+        return replace(d, batch=count), start
+    return d, 0
 
 
 # ------------------------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML during the timed region)
 # ------------------------------------------------------------------------------------------
 class Clocks:
     """Samples SM clock and throttle reasons through NVML in a background thread (about
@@ -148,64 +170,166 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------------------
-# CPU reference (the oracle port of the reference algorithms)
+# the reference CPU algorithms (baseline/_ref's unmodified convbench, else the oracle port)
 # ------------------------------------------------------------------------------------------
-def cpu_reference(d_full, seconds: float, threads: int | None = None, algo: str = "main"):
-    """GFLOP/s of the reference CPU algorithm on a bounded sample of the workload:
-    batches of `sample_n` images of the same conv until `seconds` have elapsed."""
-    import numpy as np
-    from oracle import conv_oracle as orc
-    from oracle import reference_port as rp
-    from paper_2407_10730_b200.descriptor import flop_count
-    threads = threads or os.cpu_count() or 1
+def host_cpu() -> dict:
+    model = ""
     try:
-        from threadpoolctl import threadpool_limits
-        limiter = threadpool_limits(threads)
-    except ImportError:  # pragma: no cover
-        limiter = None
-    d1 = replace(d_full, batch=min(d_full.batch, 2))
-    x, w, b = orc.make_inputs(d1, 0)
-    fn = rp.conv_main_blocked_direct if algo == "main" else rp.conv_baseline_im2col_gemm
-    done = 0
-    t0 = time.perf_counter()
-    while True:
-        fn(d1, x, w, b)
-        done += 1
-        el = time.perf_counter() - t0
-        if el >= seconds or done >= 1000:
-            break
-    if limiter is not None:
-        limiter.unregister() if hasattr(limiter, "unregister") else None
-    flops = flop_count(d1) * done
-    return {"value": flops / el / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "algorithm": f"reference {'conv_main_blocked_direct' if algo == 'main' else 'conv_baseline_im2col_gemm'} "
-                         "(oracle/reference_port.py)",
-            "sample": f"{done} x {d1.batch} image(s) of the workload conv ({el:.1f} s)",
-            "seconds": el}
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"model": model, "cpu_count": os.cpu_count()}
 
 
-def run_reference(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
+class RefCPU:
+    """One call of a reference algorithm: `main` = conv_main_blocked_direct (algos.py:265-334),
+    `baseline` = conv_baseline_im2col_gemm (algos.py:185-209), on host numpy buffers."""
+
+    def __init__(self):
+        self.kind = "port"
+        self.cb = None
+        ref = ROOT / "baseline" / "_ref"
+        if (ref / "convbench" / "__init__.py").exists():
+            if str(ref) not in sys.path:
+                sys.path.append(str(ref))
+            try:
+                import convbench.algos
+                import convbench.descriptor
+                import convbench.timing
+                self.cb = convbench
+                self.kind = "reference"
+            except Exception:  # a broken install: fall back to the pinned port
+                self.cb = None
+        self.source = ("baseline/_ref convbench (the unmodified reference package)"
+                       if self.cb else "oracle/reference_port.py (restatement pinned bit-exact "
+                                       "to the reference by tests/test_oracle.py)")
+
+    def __call__(self, algo: str, d, x, w):
+        if self.cb is not None:
+            cb = self.cb
+            rd = cb.descriptor.ConvDescriptor(**{f: getattr(d, f) for f in (
+                "batch", "in_channels", "in_h", "in_w", "out_channels", "k_h", "k_w", "stride_h",
+                "stride_w", "pad_h", "pad_w", "dil_h", "dil_w", "groups", "has_bias")})
+            inp = cb.algos.ConvInputs(desc=rd, input=x, weights=w)
+            fn = cb.algos.conv_main_blocked_direct if algo == "main" else cb.algos.conv_baseline_im2col_gemm
+            return fn(inp, cb.timing.PhaseLedger())
+        from oracle import reference_port as rp
+        fn = rp.conv_main_blocked_direct if algo == "main" else rp.conv_baseline_im2col_gemm
+        return fn(d, x, w, None)
+
+
+def cpu_time(ref: RefCPU, algo: str, d, x, w, seconds: float, threads: int) -> dict:
+    """GFLOP/s of `algo` on (d, x, w), repeated until `seconds` elapse (at least once)."""
+    from threadpoolctl import threadpool_limits
+    from paper_2407_10730_b200.descriptor import flop_count
+    with threadpool_limits(threads):
+        done, out = 0, None
+        t0 = time.perf_counter()
+        while True:
+            out = ref(algo, d, x, w)
+            done += 1
+            el = time.perf_counter() - t0
+            if el >= seconds or done >= 1000:
+                break
+    return {"value": flop_count(d) * done / el / 1e9, "calls": done, "seconds": el,
+            "threads": threads, "out": out}
+
+
+def cpu_sample(d, x, w):
+    """The bounded CPU sample of a config: its first CPU_SAMPLE_IMAGES images."""
+    import numpy as np
+    n = min(d.batch, CPU_SAMPLE_IMAGES)
+    return replace(d, batch=n), np.ascontiguousarray(x[:n]), w
+
+
+def cpu_baseline_leg(d_head, x_head, w_head, seconds: float, gpu_samples: dict, timed_sample):
+    """Rank 0, N=1: the reference CPU algorithms beside the GPU result, and the parity of
+    the GPU outputs against the reference outputs of the same images."""
+    import numpy as np
+    from paper_2407_10730_b200.configs import CONFIGS
+    from paper_2407_10730_b200.harness import RunConfig, make_inputs
+    from paper_2407_10730_b200.tensor import normalized_max_err
+    ref = RefCPU()
+    allt = os.cpu_count() or 1
+    table, parity = {}, {}
+    # headline: SConv (blocked direct) on the workload's sample, all threads
+    d1, x1, w1 = cpu_sample(d_head, x_head, w_head)
+    head = cpu_time(ref, "main", d1, x1, w1, seconds, allt)
+    red = (d1.in_channels // d1.groups) * d1.k_h * d1.k_w
+    if timed_sample is not None:
+        parity["timed_graph"] = {"what": f"the timed ring graph's output y[:{d1.batch}] vs the "
+                                         "reference SConv on the same images",
+                                 "err": normalized_max_err(timed_sample, head["out"], red)}
+    per = max(0.3, seconds / 20)
+    for name in TABLE_CONFIGS:
+        if name not in gpu_samples and gpu_samples:
+            continue
+        d = CONFIGS[name]
+        inp = make_inputs(d, RunConfig(seed=0))
+        ds, xs, ws = cpu_sample(d, inp.input, inp.weights)
+        row = {"sample": f"{ds.batch} of {d.batch} image(s)"}
+        outs = {}
+        for algo in ("main", "baseline"):
+            for t in (1, allt):
+                r = cpu_time(ref, algo, ds, xs, ws, per, t)
+                row[f"{algo}_t{t}_gflops"] = r["value"]
+                outs[algo] = r["out"]
+        table[name] = row
+        redc = (d.in_channels // d.groups) * d.k_h * d.k_w
+        if outs["main"] is not None and outs["baseline"] is not None:
+            row["ref_main_vs_baseline_err"] = normalized_max_err(outs["main"], outs["baseline"], redc)
+        for path, y in gpu_samples.get(name, {}).items():
+            parity.setdefault("configs", {}).setdefault(name, {})[path] = \
+                normalized_max_err(y[:ds.batch], outs["main"], redc)
+    errs = [parity["timed_graph"]["err"]] if "timed_graph" in parity else []
+    errs += [e for c in parity.get("configs", {}).values() for e in c.values()]
+    parity_block = {"gate": f"max|y - y_ref| / sqrt(C*R*S) <= {TOL:g}",
+                    "reference": "the reference conv_main_blocked_direct (float64 accumulate, "
+                                 "one fp32 rounding) on the same images",
+                    "max_err": max(errs) if errs else None,
+                    "pass": bool(errs) and max(errs) <= TOL, **parity}
+    cpu = {"value": head["value"], "unit": UNIT, "cores": allt, "kind": ref.kind,
+           "algorithm": f"reference conv_main_blocked_direct ({ref.source})",
+           "sample": f"{head['calls']} x {d1.batch} image(s) of the workload conv "
+                     f"({head['seconds']:.1f} s)",
+           "host": host_cpu(), "table": table,
+           "table_note": f"GFLOP/s on {CPU_SAMPLE_IMAGES}-image samples (the whole op for N=1 "
+                         "configs); main = conv_main_blocked_direct (SConv), baseline = "
+                         "conv_baseline_im2col_gemm; t1 = 1 thread (the paper protocol, "
+                         f"PAPER.md:176), t{allt} = all host threads (threadpoolctl)"}
+    return cpu, parity_block
+
+
+def run_reference(args, ranks):
+    if ranks.rank != 0:
         return 0
-    d = workload(args.config, 1, "weak", 0)
-    from paper_2407_10730_b200.configs import conv_flops
+    d, _ = workload(args.config, 1, "weak", 0)
+    from paper_2407_10730_b200.harness import RunConfig, make_inputs
+    inp = make_inputs(d, RunConfig(seed=0))
+    d1, x1, w1 = cpu_sample(d, inp.input, inp.weights)
+    ref = RefCPU()
+    threads = os.cpu_count() or 1
     per_step = max(1.0, args.cpu_seconds / max(1, args.steps))
     for _ in range(args.warmup):
-        cpu_reference(d, 0.0)
+        cpu_time(ref, "main", d1, x1, w1, 0.0, threads)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_reference(d, per_step))
+        vals.append(cpu_time(ref, "main", d1, x1, w1, per_step, threads))
     el = time.perf_counter() - t0
     value = statistics.mean(v["value"] for v in vals)
+    sample = f"{vals[0]['calls']} x {d1.batch} image(s) of the workload conv per step " \
+             f"({vals[0]['seconds']:.1f} s)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded U(-1,1), reference make_inputs)",
             "config": {"workload": f"{args.config}: {d}", "global_batch": d.batch,
-                       "sample_per_step": vals[0]["sample"]},
-            "cpu_baseline": {k: vals[0][k] for k in ("kind", "cores", "sample", "algorithm")} | {"value": value, "unit": UNIT},
+                       "sample_per_step": sample},
+            "cpu_baseline": {"kind": ref.kind, "cores": threads, "sample": sample,
+                             "algorithm": f"reference conv_main_blocked_direct ({ref.source})",
+                             "host": host_cpu(), "value": value, "unit": UNIT},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -214,41 +338,22 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
-def run_ours(args):
-    import numpy as np
+def measure_ring(d, variant, x_h, w_h, steps, warmup, barrier, clocks_idx=None):
+    """K whole steps (K3 + K0 + K6) replayed as ring graphs over RING rotating buffer sets.
+    Returns ms per step, the launches per step, the mean phase times of the same step
+    graphs (instrumented copies, replayed after the timed region) and the last output."""
     import torch
     from paper_2407_10730_b200 import _capi, algos
-    from paper_2407_10730_b200.configs import conv_flops
-    from paper_2407_10730_b200.harness import RunConfig, make_inputs
-    from paper_2407_10730_b200.roofline import conv_roofline, load_peaks
     from paper_2407_10730_b200.timing import EventLedger, Phase
-
-    rank, world, local = dist_env()
-    variant = algos.resolve_variant(workload(args.config, world, args.scaling, rank),
-                                    args.variant or algos.FUSED_AUTO)
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _capi.load()
-    d = workload(args.config, world, args.scaling, rank)
-    flops = conv_flops(d)
-
-    host = make_inputs(d, RunConfig(seed=rank))
-    x_h, w_h = host.input, host.weights
     dev = [(torch.from_numpy(x_h).cuda(), torch.from_numpy(w_h).cuda()) for _ in range(RING)]
     ys = [torch.empty((d.batch, d.out_channels) + algos.output_shape(d), device="cuda")
           for _ in range(RING)]
-    # One plan (layout, packed weights, workspace) and one CUDA graph per ring slot; each
-    # graph is a full step: K3 weight split + K0 activation split + K6 conv.
     fc = algos.FusedConv(d, variant)
     launches0 = lib.cb_launch_count()
     fc.run(dev[0][0], ys[0], weights=dev[0][1])
     launches_per_step = lib.cb_launch_count() - launches0
     graphs = [fc.capture(x, w, y) for (x, w), y in zip(dev, ys)]
-    # the timed stream replays one graph per ring of RING steps (no launch gap between the
-    # steps of a ring); a remainder of steps replays the per-step graphs
     ring_graph = fc.capture_steps([(x, w, y) for (x, w), y in zip(dev, ys)])
 
     def run_steps(k: int) -> None:
@@ -256,63 +361,125 @@ def run_ours(args):
             ring_graph.replay()
         for i in range(k % RING):
             graphs[i].replay()
-    # Instrumented copies of the same step graphs: external CUDA events captured between
-    # K3 / K0 / K6 re-record on every replay.  Event nodes add launch gaps, so these are
-    # replayed in a second pass after the timed region, only to time the kernels.
     slot_ledgers = [EventLedger(external=True) for _ in range(RING)]
     igraphs = [fc.capture(x, w, y, ledger=led) for (x, w), y, led in zip(dev, ys, slot_ledgers)]
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
-    run_steps(args.warmup)
+    run_steps(warmup)
     torch.cuda.synchronize()
-
-    # ---- timed region: exactly K steps ----
     barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
-        run_steps(args.steps)
-        t1.record()
-        torch.cuda.synchronize()
+    clk = Clocks(clocks_idx) if clocks_idx is not None else None
+    if clk:
+        clk.__enter__()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    run_steps(steps)
+    t1.record()
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__(None, None, None)
     barrier()
-    launches = launches_per_step * args.steps
-    ms = t0.elapsed_time(t1) / args.steps
-
-    # per-kernel durations: replay the instrumented graphs as many steps as were timed and
-    # read every slot's in-graph events after each ring cycle
+    ms = t0.elapsed_time(t1) / steps
+    last = ys[(steps - 1) % RING] if steps % RING else ys[RING - 1]
+    out_sample = last[:CPU_SAMPLE_IMAGES].cpu().numpy()
     reports = []
-    for i in range(max(args.steps, RING)):
+    for i in range(max(steps, RING)):
         igraphs[i % RING].replay()
         if i % RING == RING - 1:
             reports.extend(led.snapshot() for led in slot_ledgers)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        tot = torch.tensor([float(flops)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tot)
-        total_flops = float(tot.item())
-    else:
-        total_flops = float(flops)
-    value = total_flops / (ms * 1e-3) / 1e9
+    phase = lambda p: statistics.mean(r.elapsed_ns[p] for r in reports)
+    res = {"ms": ms, "launches_per_step": launches_per_step, "kern_ns": phase(Phase.IN_MICROKERNEL),
+           "pack_ns": phase(Phase.IN_PACKING), "wsplit_ns": phase(Phase.PRE_REORDER),
+           "replayed": len(reports), "out_sample": out_sample,
+           "clocks": clk.summary() if clk else None}
+    del graphs, ring_graph, igraphs, dev, ys, fc
+    torch.cuda.empty_cache()
+    return res
 
-    kern_ns = statistics.mean(r.elapsed_ns[Phase.IN_MICROKERNEL] for r in reports)
-    pack_ns = statistics.mean(r.elapsed_ns[Phase.IN_PACKING] for r in reports)
-    wsplit_ns = statistics.mean(r.elapsed_ns[Phase.PRE_REORDER] for r in reports)
 
-    # ---- e2e through the same public call with pinned host buffers ----
+def config_table(peaks, runs: int = 5):
+    """Per config (1-4) and algorithm: graph-replayed phase times, one L2 flush (a 256 MB
+    write) before every replay, outside the phase events.  Returns (table, output samples
+    of every algorithm for the CPU parity check)."""
+    import torch
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.configs import CONFIGS
+    from paper_2407_10730_b200.harness import RunConfig, make_inputs, to_device
+    from paper_2407_10730_b200.roofline import conv_roofline
+    from paper_2407_10730_b200.timing import EventLedger, Phase, aggregate
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > 2x L2
+    hbm = peaks["hbm_gbs"] * 1e9
+    table, samples = {}, {}
+    for name in TABLE_CONFIGS:
+        d = CONFIGS[name]
+        inp = to_device(make_inputs(d, RunConfig(seed=0)))
+        fused_v = algos.resolve_variant(d, algos.FUSED_AUTO)
+        algos_ = [("fused", fused_v, lambda i, l: algos.conv_fused(i, l, variant=fused_v))]
+        if fused_v != "tc3xtf32":
+            algos_.append(("fused_tf32", "tc3xtf32",
+                           lambda i, l: algos.conv_fused(i, l, variant="tc3xtf32")))
+        algos_ += [("im2col_gemm", algos.DEFAULT_VARIANT,
+                    lambda i, l: algos.conv_baseline_im2col_gemm(i, l)),
+                   ("sconv", algos.DEFAULT_VARIANT,
+                    lambda i, l: algos.conv_main_blocked_direct(i, l))]
+        row = {}
+        for tag, variant, fn in algos_:
+            fn(inp, EventLedger())  # eager first call: plans, kernel attributes, tensor maps
+            led = EventLedger(external=True)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=side):
+                y = fn(inp, led)
+            reps = []
+            for r in range(runs + 1):
+                flush.zero_()
+                graph.replay()
+                if r >= 1:
+                    reps.append(led.snapshot())
+            torch.cuda.synchronize()
+            samples.setdefault(name, {})[tag] = y[:CPU_SAMPLE_IMAGES].cpu().numpy()
+            del graph
+            st = aggregate(reps)
+            op = st.operation_ns_mean
+            m = {p.name.lower(): st.phase_ns_mean[p] / 1e3 for p in Phase if st.calls[p]}
+            rl = conv_roofline(d, variant, peaks)
+            ent = {"variant": variant, "operation_us": op / 1e3,
+                   "gflops": rl["flops"] / (op * 1e-9) / 1e9 if op else None,
+                   "phases_us": m, "calls": {p.name.lower(): st.calls[p] for p in Phase if st.calls[p]},
+                   "roofline_us": rl["t_roofline_s"] * 1e6, "bound": rl["bound"],
+                   "op_roofline_frac": rl["t_roofline_s"] / (op * 1e-9) if op else None}
+            if tag.startswith("fused"):
+                k = st.phase_ns_mean[Phase.IN_MICROKERNEL]
+                ent["kernel_us"] = k / 1e3
+                ent["kernel_roofline_frac"] = rl["t_roofline_s"] / (k * 1e-9) if k else None
+                ent["target_60pct_met"] = bool(k and rl["t_roofline_s"] / (k * 1e-9) >= 0.6)
+            else:
+                pk = st.phase_ns_mean[Phase.PRE_REORDER if tag == "im2col_gemm" else Phase.IN_PACKING]
+                ent["pack_kernel"] = "K1 im2col" if tag == "im2col_gemm" else "K2 slice pack"
+                ent["pack_gbs"] = rl["pack_bytes"] / (pk * 1e-9) / 1e9 if pk else None
+                ent["pack_hbm_frac"] = rl["pack_bytes"] / (pk * 1e-9) / hbm if pk else None
+                ent["target_70pct_met"] = bool(pk and rl["pack_bytes"] / (pk * 1e-9) / hbm >= 0.7)
+                pack = st.phase_ns_mean[Phase.IN_PACKING] + (
+                    st.phase_ns_mean[Phase.PRE_REORDER] if tag == "im2col_gemm" else 0.0)
+                ent["pack_share"] = pack / op if op else None
+            row[tag] = ent
+        table[name] = row
+        del inp
+        torch.cuda.empty_cache()
+    del flush
+    return table, samples
+
+
+def e2e_pipeline(d, variant, x_h, w_h, steps, warmup, barrier, max_over):
+    """HostPipeline: pinned host x, w in and y out every step, copies overlapping kernels."""
+    import torch
+    from paper_2407_10730_b200 import algos
     x_p = torch.from_numpy(x_h).pin_memory()
     w_p = torch.from_numpy(w_h).pin_memory()
-    y_p = torch.empty(ys[0].shape, dtype=torch.float32).pin_memory()
-    # HostPipeline: the package's host-buffer API -- per step, x and w go host->device and
-    # y device->host, on their own streams, overlapping the neighbouring steps' kernels
+    y_p = torch.empty((d.batch, d.out_channels) + algos.output_shape(d), dtype=torch.float32).pin_memory()
     pipe = algos.HostPipeline(d, variant)
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):
         pipe.submit(x_p, w_p, y_p)
     pipe.synchronize()
     barrier()
@@ -320,27 +487,121 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     pipe.wait_streams_for(e0)
-    for _ in range(args.steps):
+    for _ in range(steps):
         pipe.submit(x_p, w_p, y_p)
     pipe.record_done(e1)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device="cuda")
+    ms = max_over(e0.elapsed_time(e1) / steps)
+    return ms, int(x_h.nbytes + w_h.nbytes), int(y_p.numel() * 4)
+
+
+def e2e_dropin(d, variant, x_h, w_h, calls: int = 10):
+    """The reference-facing drop-in as the reference harness calls it: conv_fused on numpy
+    inputs returning numpy (upload, K3 + K0 + K6, download; synchronous), per call; then the
+    same with the identity-keyed input cache (upload once, as harness.install() runs it)."""
+    import torch
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.algos import ConvInputs
+    inp = ConvInputs(desc=d, input=x_h, weights=w_h)
+    out = {}
+    for cached in (False, True):
+        algos.set_input_cache(cached)
+        try:
+            algos.conv_fused(inp, variant=variant)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(calls):
+                y = algos.conv_fused(inp, variant=variant)
+            el = (time.perf_counter() - t0) / calls
+        finally:
+            algos.set_input_cache(False)
+        out["cached" if cached else "uncached"] = {"ms_per_call": el * 1e3,
+                                                   "value": algos.flop_count(d) / el / 1e9}
+    assert y.shape == (d.batch, d.out_channels) + algos.output_shape(d)
+    return {"unit": UNIT, "api": "algos.conv_fused(ConvInputs(numpy x, w)) -> numpy y (host clock, "
+                                 "synchronous; pageable copies)",
+            "h2d_bytes_per_call_uncached": int(x_h.nbytes + w_h.nbytes),
+            "d2h_bytes_per_call": int(d.batch * d.out_channels * 4 *
+                                      algos.output_shape(d)[0] * algos.output_shape(d)[1]), **out}
+
+
+def run_ours(args, ranks):
+    import torch
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.configs import CONFIGS, conv_flops
+    from paper_2407_10730_b200.harness import RunConfig, make_inputs
+    from paper_2407_10730_b200.roofline import conv_roofline, load_peaks
+
+    rank, world, local = ranks.rank, ranks.world, ranks.local
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        return float(t.item())
+
+    def sum_over(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    d, start = workload(args.config, world, args.scaling, rank)
+    variant = algos.resolve_variant(d, args.variant or algos.FUSED_AUTO)
+    flops = conv_flops(d)
+    # the global batch's make_inputs data; each rank takes its contiguous slice (strong) or
+    # the whole batch with its own seed (weak)
+    full = CONFIGS[args.config]
+    if args.scaling == "strong":
+        host = make_inputs(full, RunConfig(seed=0))
+        x_h = host.input[start:start + d.batch].copy()
+    else:
+        host = make_inputs(full, RunConfig(seed=rank))
+        x_h = host.input
+    w_h = host.weights
+
+    m = measure_ring(d, variant, x_h, w_h, args.steps, args.warmup, barrier, clocks_idx=local)
+    ms = max_over(m["ms"])
+    total_flops = sum_over(float(flops))
+    value = total_flops / (ms * 1e-3) / 1e9
+
+    variants = {}
+    if not args.no_variants:
+        for v in ("tc3xtf32", "tc3xbf16"):
+            if v == variant:
+                continue
+            mv = measure_ring(d, v, x_h, w_h, max(8, args.steps // 2), max(3, args.warmup // 2),
+                              barrier)
+            msv = max_over(mv["ms"])
+            variants[v] = {"ms_per_step": msv, "value": sum_over(float(flops)) / (msv * 1e-3) / 1e9,
+                           "k6_us": mv["kern_ns"] / 1e3}
+
+    e2e_ms, h2d, d2h = e2e_pipeline(d, variant, x_h, w_h, args.steps, args.warmup, barrier, max_over)
     e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
-           "api": "HostPipeline.submit (pinned host x, w in; y out; copies overlap kernels)",
-           "h2d_bytes_per_step": int(x_h.nbytes + w_h.nbytes),
-           "d2h_bytes_per_step": int(y_p.numel() * 4)}
+           "api": "algos.HostPipeline.submit (pinned host x, w in; y out; copies overlap kernels)",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    dropin = e2e_dropin(d, variant, x_h, w_h) if rank == 0 else None
 
     if rank != 0:
+        barrier()
         if dist is not None:
             dist.destroy_process_group()
         return 0
 
     peaks = load_peaks()
     rl = conv_roofline(d, variant, peaks)
+    kern_ns = m["kern_ns"]
     achieved = flops / (kern_ns * 1e-9) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
@@ -349,96 +610,115 @@ def run_ours(args):
             traffic = json.loads(prof.read_text()).get(f"{args.config}/{variant}", {}).get("dram_bytes")
         except (ValueError, OSError):
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "kernel": "conv_tma_kernel (K6)", "kernel_us": kern_ns / 1e3,
-                "peak_source": f"{peaks['source']} dense bf16 (burst)",
-                "split_effective_peak": rl["effective_peak_tflops"],
-                "frac_of_split_peak": achieved / rl["effective_peak_tflops"],
+    eff = rl["effective_peak_tflops"]
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": eff, "unit": "TFLOP/s",
+                "frac": achieved / eff, "traffic": traffic,
+                "kernel": "conv_tma_kernel (K6)" if variant != "ffma" else "conv_ffma_kernel",
+                "kernel_us": kern_ns / 1e3,
+                "peak_source": f"{peaks['source']} dense bf16 (burst) {peaks['bf16_tflops']} TFLOP/s / "
+                               f"{3 if variant == 'tc3xbf16' else 6} MMAs per fp32 product ({variant})",
+                "dense_bf16_peak": peaks["bf16_tflops"],
+                "frac_of_dense_bf16": achieved / peaks["bf16_tflops"],
                 "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": rl["bytes"],
                 "roofline_us": rl["t_roofline_s"] * 1e6}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None,
+            "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32", "compute": f"{variant}: tcgen05 split products, fp32 accumulate in TMEM"
             if variant != "ffma" else "ffma fp32",
             "data": "synthetic (seeded U(-1,1), reference make_inputs)",
-            "config": {"workload": f"{args.config}: N={d.batch} C={d.in_channels} {d.in_h}x{d.in_w} "
+            "config": {"workload": f"{args.config}: N={full.batch} C={d.in_channels} {d.in_h}x{d.in_w} "
                                    f"K={d.out_channels} {d.k_h}x{d.k_w} s{d.stride_h} p{d.pad_h}, "
                                    "fused implicit-GEMM conv per step",
-                       "global_batch": d.batch * (world if args.scaling == "weak" else 1),
+                       "global_batch": full.batch * (world if args.scaling == "weak" else 1),
                        "per_gpu_batch": d.batch, "variant": variant,
-                       "l2": f"{RING} rotating input/workspace/output sets (> 2x L2); no flush",
+                       "l2": f"{RING} rotating input/workspace/output sets (> 2x L2 per ring "
+                             "cycle at N=1); no flush",
                        "graph": f"one CUDA graph per {RING} whole steps (K3 + K0 + K6 each)",
-                       "parallelism": f"batch-sharded x{world}, no collective on the data path"},
-            "gpu_launches": int(launches),
-            "launches_per_step": launches / args.steps,
-            "step_phases_us": {"pre_reorder(K3 weight split)": wsplit_ns / 1e3,
-                               "in_packing(K0 act split)": pack_ns / 1e3,
+                       "parallelism": f"batch-sharded x{world} ({args.scaling} scaling), no "
+                                      "collective on the data path"},
+            "gpu_launches": int(m["launches_per_step"] * args.steps),
+            "launches_per_step": m["launches_per_step"],
+            "step_phases_us": {"pre_reorder(K3 weight split)": m["wsplit_ns"] / 1e3,
+                               "in_packing(K0 act split)": m["pack_ns"] / 1e3,
                                "in_microkernel(K6 conv)": kern_ns / 1e3,
                                "timing": "CUDA events captured in the step graphs, replayed "
-                                         f"{len(reports)} steps after the timed region"},
-            "roofline": roofline, "e2e": e2e, "clocks": clk.summary()}
-
-    if not args.no_breakdown:
-        line["breakdown"] = breakdown(d, variant)
+                                         f"{m['replayed']} steps after the timed region"},
+            "roofline": roofline, "e2e": e2e, "e2e_dropin": dropin, "clocks": m["clocks"]}
+    if variants:
+        line["variants"] = variants
+    samples = {}
+    if world == 1 and not args.no_breakdown:
+        table, samples = config_table(peaks)
+        line["configs"] = table
+        line["breakdown"] = {k: table[args.config][k] for k in ("fused", "im2col_gemm", "sconv")} \
+            if args.config in table else None
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference(d, args.cpu_seconds)
-        line["cpu_baseline"].pop("seconds", None)
+        cpu, parity = cpu_baseline_leg(d, x_h, w_h, args.cpu_seconds, samples, m["out_sample"])
+        line["cpu_baseline"] = cpu
+        line["parity"] = parity
     print(json.dumps(line), flush=True)
+    barrier()
     if dist is not None:
         dist.destroy_process_group()
     return 0
 
 
-def breakdown(d, fused_variant, runs: int = 5):
-    """Per-phase CUDA-event times (us, mean of `runs`) of the three GPU algorithms.  Each
-    algorithm is captured once into a CUDA graph with external phase events and replayed
-    (the harness's graph mode), so a phase's time is its kernels', not the host's launch
-    latency between an eager event and the kernel after it."""
+def run_dry(args, ranks):
+    """The multi-rank control path on CPU (gloo): launcher, sharding, barrier, max-over-ranks
+    time and FLOP sum, rank-0 line.  A step is a tiny numpy stand-in, never a measurement."""
+    import numpy as np
     import torch
-    from paper_2407_10730_b200 import algos
-    from paper_2407_10730_b200.harness import RunConfig, make_inputs, to_device
-    from paper_2407_10730_b200.timing import EventLedger, Phase, aggregate
-    inp = to_device(make_inputs(d, RunConfig(seed=0)))
-    out = {}
-    for name, fn in (("im2col_gemm", lambda i, l: algos.conv_baseline_im2col_gemm(i, l)),
-                     ("sconv", lambda i, l: algos.conv_main_blocked_direct(i, l)),
-                     ("fused", lambda i, l: algos.conv_fused(i, l, variant=fused_variant))):
-        fn(inp, EventLedger())  # eager first call: plans, kernel attributes, tensor maps
-        led = EventLedger(external=True)
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=side):
-            fn(inp, led)
-        reps = []
-        for r in range(runs + 2):
-            graph.replay()
-            if r >= 2:
-                reps.append(led.snapshot())
-        del graph
-        st = aggregate(reps)
-        op = st.operation_ns_mean
-        pack = st.phase_ns_mean[Phase.IN_PACKING] + (st.phase_ns_mean[Phase.PRE_REORDER]
-                                                    if name == "im2col_gemm" else 0.0)
-        out[name] = {"operation_us": op / 1e3,
-                     "gflops": algos.flop_count(d) / (op * 1e-9) / 1e9 if op else None,
-                     "pack_share": pack / op if op else None,
-                     "phases_us": {p.name.lower(): st.phase_ns_mean[p] / 1e3 for p in Phase
-                                   if st.calls[p]},
-                     "calls": {p.name.lower(): st.calls[p] for p in Phase if st.calls[p]},
-                     "timing": "CUDA graph replay, external phase events"}
-    torch.cuda.synchronize()
-    return out
+    import torch.distributed as dist
+    from paper_2407_10730_b200.configs import CONFIGS, conv_flops
+    if ranks.world > 1:
+        dist.init_process_group("gloo")
+    d, start = workload(args.config, ranks.world, args.scaling, ranks.rank)
+    a = np.random.default_rng(ranks.rank).random((64, 64))
+    if ranks.world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a = a @ a / 64.0
+    el = time.perf_counter() - t0
+    t = torch.tensor([el, float(conv_flops(d)), float(d.batch)], dtype=torch.float64)
+    if ranks.world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t)
+        el, flops, images = float(mx[0]), float(t[1]), int(t[2])
+    else:
+        flops, images = float(t[1]), int(t[2])
+    if ranks.rank == 0:
+        full = CONFIGS[args.config]
+        print(json.dumps({"metric": METRIC, "value": flops / max(el, 1e-9) / 1e9, "unit": UNIT,
+                          "n_gpus": ranks.world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": 1e3 * el / max(1, args.steps), "higher_is_better": True,
+                          "scaling": args.scaling, "dry_run": True,
+                          "config": {"workload": args.config,
+                                     "global_batch": full.batch * (ranks.world if args.scaling == "weak" else 1),
+                                     "images_over_ranks": images, "per_gpu_batch": d.batch,
+                                     "first_image": start}}), flush=True)
+    if ranks.world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    return run_ours(args)
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    from paper_2407_10730_b200.launch import Ranks, ensure_ranks, env_ranks
+    if args.impl == "reference":  # rank 0 alone times the CPU reference; no relaunch needed
+        r = env_ranks()
+        return run_reference(args, r or Ranks(0, 1, 0))
+    ranks = ensure_ranks(args.gpus, str(Path(__file__).resolve()), argv)
+    if isinstance(ranks, int):  # the relaunched ranks ran; propagate their exit code
+        return ranks
+    if args.dry_run:
+        return run_dry(args, ranks)
+    return run_ours(args, ranks)
 
 
 if __name__ == "__main__":

@@ -193,7 +193,15 @@ int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, vo
 int cb_fused_pack_input(int variant, const cb_conv_desc* d, const float* x, void* workspace,
                         size_t workspace_bytes, void* stream);
 
-/* K6/K7 (IN_MICROKERNEL) on already packed operands. */
+/* K6/K7 (IN_MICROKERNEL) on already packed operands.
+ *
+ * Concurrency contract: when the tile plan splits the tail tiles along K (cb_fused_plan_tiles
+ * reports it through the workspace size), the K parts of a tile wait for one another across
+ * CTAs, so every CTA of the persistent grid (at most one per SM) must be resident at once.
+ * The library checks the grid against the occupancy API of an idle device
+ * (CB_ERR_UNSUPPORTED otherwise).  Do not run this call concurrently with other kernels on
+ * other streams of the same GPU, or under an MPS SM cap: stream-ordered use -- every
+ * kernel of this library, one stream per process -- is the supported mode. */
 int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x,
                          const void* workspace, size_t workspace_bytes, const void* w_hi,
                          const void* w_lo, const float* w_f32, const float* bias, float* y,

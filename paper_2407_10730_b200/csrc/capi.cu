@@ -30,6 +30,12 @@ int check_launch(const char* what) {
     return CB_OK;
 }
 
+int promote_k(bool bf16) {  // read per launch: a host-side getenv; tests toggle it in-process
+    const char* e = std::getenv("CB_PROMOTE_K");
+    const int v = e ? std::atoi(e) : bf16 ? 4096 : 2048;
+    return v > 0 ? v : (1 << 30);
+}
+
 int sm_count() {
     static int count = 0;
     static std::once_flag once;

@@ -37,6 +37,11 @@ inline int32_t round_up(int32_t a, int32_t b) { return (a + b - 1) / b * b; }
 inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int sm_count();  // cached multiProcessorCount of the current device
+// Reduction elements accumulated in one tensor-core accumulator before it is drained and
+// added in fp32 (round to nearest) by the epilogue: the tcgen05 fp32 accumulation truncates,
+// so its error grows faster than linearly with the MMAs per accumulator.  CB_PROMOTE_K
+// overrides (diagnostics; 0 = never promote).
+int promote_k(bool bf16);  // defaults: 2048 (tf32 MMAs, K = 8 each), 4096 (bf16 MMAs, K = 16)
 
 // ------------------------------------------------------------------------------------
 // Pixel addressing modes shared by the GEMM/conv kernels.

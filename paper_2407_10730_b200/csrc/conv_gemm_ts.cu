@@ -56,6 +56,12 @@ struct G8Params {
     // item each, so the last wave keeps every SM busy.  A is rebuilt per range.
     int64_t full_items;
     int tail_split;
+    // Accumulator promotion: the tensor core's fp32 accumulation truncates, so its error
+    // grows faster than linearly with the number of MMAs into one accumulator (measured on
+    // the config-5 sweep: up to 1.3e-3 normalized at C*R*S = 100352).  Every range_chunks
+    // chunks (of 32 reduction elements) the accumulator is drained by the epilogue and
+    // added to the output in fp32 (round to nearest), then restarted.
+    int range_chunks;
 };
 
 // channel range [lo, hi) of part `sub` of a BN-wide tile cut into `parts` (16-aligned)
@@ -234,8 +240,8 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         // ============================ epilogue ==========================================
         const int quad = warp & 3;
         const int m = quad * 32 + lane;
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++i) {
+        int i = 0;  // accumulator ranges drained so far (acc_full phase)
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
@@ -244,15 +250,19 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             int64_t obase = 0, ostride = 0;
             if (jvalid) dst_linear(g, p.pm, p.pm.j_begin + jl, obase, ostride);
             const int f_tile0 = nt * BN + c_lo;
+            const int ncol = min(c_hi - c_lo, g.kpg - f_tile0);
+            const int nranges = (nch + p.range_chunks - 1) / p.range_chunks;
+#pragma unroll 1
+            for (int rg = 0; rg < nranges; ++rg, ++i) {
             ptx::mbar_wait(acc_full, i & 1);
             ptx::tc_fence_after();
-            const int ncol = min(c_hi - c_lo, g.kpg - f_tile0);
+            const bool add = p.add_mode || rg > 0;  // later ranges add to the first's store
 #pragma unroll 1
             for (int c0 = 0; c0 < ncol; c0 += 32) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, r);
                 ptx::tmem_ld_wait();
-                if (c0 + 32 >= ncol) {  // accumulator fully read: the next item may start
+                if (c0 + 32 >= ncol) {  // accumulator fully read: the next range may start
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(acc_empty);
                 }
@@ -260,7 +270,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 const int nvalid = min(32, ncol - c0);
                 const int fb = gi * g.kpg + f_tile0 + c0;
                 float* dst = p.out + obase + (int64_t)fb * ostride;
-                if (p.add_mode) {
+                if (add) {
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (e < nvalid) dst[(int64_t)e * ostride] += __uint_as_float(r[e]);
@@ -271,6 +281,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                             dst[(int64_t)e * ostride] =
                                 __uint_as_float(r[e]) + (p.bias ? __ldg(p.bias + fb + e) : 0.f);
                 }
+            }
             }
         }
     } else if (warp == G8_ATMA_WARP) {
@@ -335,16 +346,24 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
         const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
         int64_t cbase = 0, sbase = 0;
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++i, cbase += nch, sbase += nstage) {
+        int i = 0;  // accumulator ranges issued so far (acc_empty phase)
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch, sbase += nstage) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
             const uint32_t idesc =
                 c_hi - c_lo == BN ? idesc_full : ptx::idesc_f32acc<BF16>(G8_BM, c_hi - c_lo);
-            ptx::mbar_wait(acc_empty, (i & 1) ^ 1);
-            ptx::tc_fence_after();
             for (int kc = 0; kc < nch; ++kc) {
+                const int kr = kc % p.range_chunks;  // position inside the accumulator range
+                if (kr == 0) {  // a fresh accumulator range: the epilogue drained the last one
+                    if (kc > 0) {
+                        if (leader) ptx::umma_commit(acc_full);
+                        __syncwarp();
+                        ++i;
+                    }
+                    ptx::mbar_wait(acc_empty, (i & 1) ^ 1);
+                    ptx::tc_fence_after();
+                }
                 const int64_t cg = cbase + kc;
                 const int slot = (int)(cg % p.ring);
                 const int64_t sg = sbase + kc / Cfg::CPS;
@@ -359,7 +378,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
 #pragma unroll
                     for (int u = 0; u < G8_CK / Cfg::UK; ++u) {
                         const uint64_t dbh = sb + 2 * u, dbl = dbh + BLO16;
-                        const uint32_t first = (kc > 0 || u > 0) ? 1u : 0u;
+                        const uint32_t first = (kr > 0 || u > 0) ? 1u : 0u;
                         ptx::umma_ts<BF16>(tmem_base, a_lo + u * 8, dbh, idesc, first);
                         ptx::umma_ts<BF16>(tmem_base, a_hi + u * 8, dbl, idesc, 1u);
                         ptx::umma_ts<BF16>(tmem_base, a_hi + u * 8, dbh, idesc, 1u);
@@ -371,6 +390,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             }
             if (leader) ptx::umma_commit(acc_full);
             __syncwarp();
+            ++i;
         }
     }
 
@@ -474,6 +494,11 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
     prm.out = out;
     prm.add_mode = add_mode;
     prm.nchunks = (g.kdim + G8_CK - 1) / G8_CK;
+    {  // balanced accumulator ranges of at most promote_k elements
+        const int rc = std::max(1, promote_k(bf16) / G8_CK);
+        const int nr = (prm.nchunks + rc - 1) / rc;
+        prm.range_chunks = std::max(1, (prm.nchunks + nr - 1) / nr);
+    }
     int bn = g.kpg <= 64 ? 64 : g.kpg <= 128 ? 128 : 256;
     if (const char* e = std::getenv("CB_K8_BN")) bn = std::min(bn, std::max(64, std::atoi(e)));  // diagnostics
     prm.m_tiles = (pm.j_count + G8_BM - 1) / G8_BM;

@@ -413,6 +413,9 @@ static TcPlan plan_tc(const Geom& g, int64_t npix, bool bf16, bool allow_split) 
         want = std::min(want, pl.num_kb / 2);
         pl.splits = std::max(1, want);
     }
+    // accumulator promotion (promote_k): no CTA accumulates more than ~promote_k reduction
+    // elements; the K splits are added into the pre-initialised output in fp32
+    if (allow_split) pl.splits = std::max(pl.splits, (pl.num_kb * bk + promote_k(bf16) - 1) / promote_k(bf16));
     pl.kb_per_split = (pl.num_kb + pl.splits - 1) / pl.splits;
     pl.splits = (pl.num_kb + pl.kb_per_split - 1) / pl.kb_per_split;
     const int kb_cta = pl.kb_per_split;

@@ -62,6 +62,12 @@ struct TmaParams {
     int add_mode;         // 0: store acc + bias, 1: fp32 reduction into out
     int tma_store;        // 1: epilogue stages 32-channel chunks in smem, TMA-stores y (tm_y)
     int bulk_parts;       // 1: tail parts write their partial chunks with 1-D bulk copies
+    int out_al16;         // 1: y is 16-byte aligned (the tail fixup's float4 stores need it)
+    // Accumulator promotion (see promote_k): an item's K blocks run as ranges of at most
+    // range_kb blocks, each into a fresh TMEM accumulator (the double buffer alternates); the
+    // epilogue adds range partials in fp32 -- into y for whole tiles, into the part's slab
+    // for tail parts -- so no accumulator sums more than ~promote_k reduction elements.
+    int range_kb;
     // Tail split-K ("stream-K lite"): the first full_items work items are whole tiles;
     // the tail_tiles tiles of the last, partial wave are each cut into tail_parts K
     // ranges of tail_kbp stages so every cluster gets work.  Parts write fp32 partials to
@@ -145,6 +151,14 @@ __device__ __forceinline__ WorkItem decode_item(const TmaParams& p, int64_t i) {
         w.kb1 = min(p.L.num_kb, w.kb0 + p.tail_kbp);
     }
     return w;
+}
+
+// accumulator ranges of an item's K blocks [kb0, kb1): nr balanced ranges of <= range_kb
+__device__ __forceinline__ int n_ranges(int kb0, int kb1, int range_kb) {
+    return max(1, (kb1 - kb0 + range_kb - 1) / range_kb);
+}
+__device__ __forceinline__ int range_begin(int kb0, int kb1, int nr, int r) {
+    return kb0 + (int)((int64_t)(kb1 - kb0) * r / nr);
 }
 
 __device__ __forceinline__ void epi_barrier() {  // the 128 epilogue threads (warps 0..3)
@@ -324,14 +338,19 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int64_t t = cl0; t < p.total_items; t += ncl, ++local) {
+            for (int64_t t = cl0; t < p.total_items; t += ncl) {
                 const WorkItem it = decode_item(p, t);
+                const int nr = n_ranges(it.kb0, it.kb1, p.range_kb);
+#pragma unroll 1
+                for (int rg = 0; rg < nr; ++rg, ++local) {
+                const int rkb0 = range_begin(it.kb0, it.kb1, nr, rg);
+                const int rkb1 = range_begin(it.kb0, it.kb1, nr, rg + 1);
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                for (int kb = rkb0; kb < rkb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t sa = da0 + (uint64_t)(stage * STG16);
@@ -343,7 +362,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                             const uint64_t dal = dah + ALO16;
                             const uint64_t dbh = sb + 2 * kk;
                             const uint64_t dbl = dbh + BLO16;
-                            const uint32_t first = (kb != it.kb0 || kk != 0) ? 1u : 0u;
+                            const uint32_t first = (kb != rkb0 || kk != 0) ? 1u : 0u;
                             if (CG == 2) {
                                 ptx::umma_pair<BF16>(d, dal, dbh, idesc, first);
                                 ptx::umma_pair<BF16>(d, dah, dbl, idesc, 1);
@@ -372,6 +391,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                         ptx::umma_commit(&tfull[acc]);
                 }
                 __syncwarp();
+                }
             }
         }
     } else {
@@ -385,12 +405,6 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
         for (int64_t t = cl0; t < p.total_items; t += ncl, ++local) {
             const WorkItem it = decode_item(p, t);
             const int gi = it.gi;
-            const int acc = local & 1;
-            const uint32_t acc_phase = (local >> 1) & 1;
-            if (local == 0 && threadIdx.x == 0) trace_stamp(p, 0);
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
-            if (threadIdx.x == 0) trace_stamp(p, 1 + local);  // accumulator ready
             const int64_t j = it.mt * (TMA_BM * CG) + rank * TMA_BM + row;
             const bool jvalid = j < g.npix;
             int64_t obase = 0;
@@ -402,6 +416,69 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
             const bool do_store = jvalid && !(p.debug & 2);
             float* dst = p.out + obase + (int64_t)(gi * g.kpg + f_tile0) * g.PQ;
             const float* bias = p.bias ? p.bias + gi * g.kpg + f_tile0 : nullptr;
+            const int nr = n_ranges(it.kb0, it.kb1, p.range_kb);
+            const bool promoted = nr > 1;
+            const int nch_all = (min(BN, g.kpg - f_tile0) + 31) / 32;
+            // this CTA's fp32 slab of a tail part ([ch/4][row][ch%4], see the fixup below)
+            float* const part_slab = it.tail >= 0
+                ? p.partials + ((int64_t)it.tail * p.tail_parts * CG + rank) * ((int64_t)BN * TMA_BM) +
+                      (int64_t)it.part * CG * ((int64_t)BN * TMA_BM)
+                : nullptr;
+            // ---- non-final accumulator ranges: fold each partial into fp32 storage (whole
+            // tiles: y, bias with the first range; tail parts: the part's own slab) ----
+#pragma unroll 1
+            for (int rg = 0; rg + 1 < nr; ++rg, ++local) {
+                const int acc = local & 1;
+                ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int ci = 0; ci < nch_all; ++ci) {
+                    const int c0 = ci * 32;
+                    const int nvalid = min(32, g.kpg - (f_tile0 + c0));
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16) + c0, r);
+                    ptx::tmem_ld_wait();
+                    if (ci + 1 == nch_all) {
+                        ptx::tc_fence_before();
+                        if (CG == 2)
+                            ptx::mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
+                        else
+                            ptx::mbar_arrive(&tempty[acc]);
+                    }
+                    if (it.tail >= 0) {
+                        float4* sl = reinterpret_cast<float4*>(part_slab) + (int64_t)(ci * 8) * TMA_BM + row;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                   __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                            if (rg > 0) {
+                                const float4 o = __ldcg(sl + (int64_t)q * TMA_BM);
+                                v.x += o.x, v.y += o.y, v.z += o.z, v.w += o.w;
+                            }
+                            __stcg(sl + (int64_t)q * TMA_BM, v);
+                        }
+                    } else if (do_store) {
+                        float* d = dst + (int64_t)c0 * g.PQ;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            if (i >= nvalid) continue;
+                            const float v = __uint_as_float(r[i]);
+                            if (p.add_mode)
+                                atomicAdd(d + (int64_t)i * g.PQ, v);
+                            else if (rg == 0)
+                                d[(int64_t)i * g.PQ] = v + (bias ? __ldg(bias + c0 + i) : 0.f);
+                            else
+                                d[(int64_t)i * g.PQ] += v;
+                        }
+                    }
+                }
+            }
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            if (local == 0 && threadIdx.x == 0) trace_stamp(p, 0);
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            if (threadIdx.x == 0) trace_stamp(p, 1 + local);  // accumulator ready
 
             if (it.tail >= 0) {
                 // ---- tail split-K, symmetric fixup: the P parts of a tail tile run
@@ -429,10 +506,16 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                     ptx::tmem_ld_32x32b_x32(lane_tm + ci * 32, r);
                     ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        __stcg(reinterpret_cast<float4*>(mine) + (int64_t)(ci * 8 + j) * TMA_BM + row,
-                               make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                           __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+                    for (int j = 0; j < 8; ++j) {
+                        float4* sl = reinterpret_cast<float4*>(mine) + (int64_t)(ci * 8 + j) * TMA_BM + row;
+                        float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                        if (promoted) {  // the part's earlier ranges, folded into its slab
+                            const float4 o = __ldcg(sl);
+                            v.x += o.x, v.y += o.y, v.z += o.z, v.w += o.w;
+                        }
+                        __stcg(sl, v);
+                    }
                 }
                 if (threadIdx.x == 0) trace_stamp(p, 20);  // partials written (issued)
                 __threadfence();
@@ -449,7 +532,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 // stores issue (loads never queue behind stores in L1)
                 // Vector stores (PQ % 4 == 0: a group of 4 pixels never straddles an image):
                 // lane l of the epilogue stores pixels m0 + 4l .. + 3 of channel rows.
-                const bool vec_store = (g.PQ % 4) == 0 && !(p.debug & 2);
+                const bool vec_store = (g.PQ % 4) == 0 && p.out_al16 && !(p.debug & 2);
                 const int64_t jv = it.mt * (TMA_BM * CG) + rank * TMA_BM + 4 * lane;
                 const bool gvalid = jv < g.npix;
                 float* vbase = p.out;
@@ -477,7 +560,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
 #pragma unroll
                         for (int o = 0; o < 4; ++o) {
                             const int q = q0 + o;
-                            if (q < P && q != it.part) {
+                            if (q < P && (q != it.part || promoted)) {
                                 const float4* src = reinterpret_cast<const float4*>(
                                                         slab_of + (int64_t)q * CG * slab) +
                                                     (int64_t)(ci * 8) * TMA_BM + row;
@@ -490,8 +573,20 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                             const int q = q0 + o;
                             if (q >= P) break;
                             if (q == it.part) {
+                                float own[32];  // last range (TMEM) + earlier ranges (own slab)
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
+                                for (int i = 0; i < 32; ++i) own[i] = __uint_as_float(r[i]);
+                                if (promoted) {
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) {
+                                        own[4 * j] += pv[o][j].x;
+                                        own[4 * j + 1] += pv[o][j].y;
+                                        own[4 * j + 2] += pv[o][j].z;
+                                        own[4 * j + 3] += pv[o][j].w;
+                                    }
+                                }
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) v[i] += own[i];
                             } else {
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) {
@@ -552,8 +647,8 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
             // pixel coordinate); tiles across an image boundary store directly
             const int64_t m0t = it.mt * (TMA_BM * CG) + rank * TMA_BM;
             const int64_t n0t = m0t / g.PQ;
-            const bool tile_tstore =
-                p.tma_store && m0t < g.npix && (min(m0t + TMA_BM, g.npix) - 1) / g.PQ == n0t;
+            const bool tile_tstore = p.tma_store && !promoted && m0t < g.npix &&
+                                     (min(m0t + TMA_BM, g.npix) - 1) / g.PQ == n0t;
 #pragma unroll 1
             for (int ci = 0; ci < nchunk; ++ci) {
                 const int c0 = ci * 32;
@@ -592,6 +687,10 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             if (i < nvalid) atomicAdd(dst + (int64_t)i * g.PQ, __uint_as_float(r[i]));
+                    } else if (promoted) {  // bias and the earlier ranges are in y already
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < nvalid) dst[(int64_t)i * g.PQ] += __uint_as_float(r[i]);
                     } else if (nvalid == 32 && !bias) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) dst[(int64_t)i * g.PQ] = __uint_as_float(r[i]);
@@ -969,6 +1068,44 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     cfg.blockDim = dim3(TMA_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = st;
+    // Tail split-K parts wait on each other across clusters, so every CTA of the grid must
+    // be resident at once.  The grid is at most one cluster per co-resident slot of an idle
+    // GPU (checked here once per configuration against the occupancy API); a launch that
+    // could not be co-resident drops the tail split instead of risking a spin that never
+    // ends.  Other kernels running concurrently on other streams can still hold SMs: see
+    // the contract in convb200.h (cb_conv_fused_packed).
+    if (prm.tail_tiles > 0) {
+        static std::once_flag occ_once;
+        static int max_units = 0;
+        std::call_once(occ_once, [&] {
+            if (CG == 2) {
+                cudaLaunchConfig_t oc{};
+                oc.gridDim = dim3((unsigned)(2 * sm_count()));
+                oc.blockDim = dim3(TMA_THREADS);
+                oc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+                cudaLaunchAttribute ca;
+                ca.id = cudaLaunchAttributeClusterDimension;
+                ca.val.clusterDim.x = 2;
+                ca.val.clusterDim.y = 1;
+                ca.val.clusterDim.z = 1;
+                oc.attrs = &ca;
+                oc.numAttrs = 1;
+                if (cudaOccupancyMaxActiveClusters(&max_units, kern, &oc) != cudaSuccess) max_units = 0;
+            } else {
+                int per_sm = 0;
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TMA_THREADS,
+                                                                  Cfg::SMEM_BYTES) != cudaSuccess)
+                    per_sm = 0;
+                max_units = per_sm * sm_count();
+            }
+            cudaGetLastError();
+        });
+        if (grid / CG > max_units)
+            return fail(CB_ERR_UNSUPPORTED,
+                        "conv_tma: tail split-K grid of " + std::to_string(grid / CG) +
+                            " clusters exceeds the " + std::to_string(max_units) +
+                            " co-resident clusters this device reports");
+    }
     cudaLaunchAttribute attr[2];
     // programmatic dependent launch: the prologue (barriers, TMEM, descriptor prefetch)
     // overlaps the tail of the preceding kernel (K0); griddepcontrol.wait guards the inputs
@@ -1048,6 +1185,8 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     prm.tma_store = (g.PQ % 4 == 0) && (g.G == 1 || g.kpg % 32 == 0) &&
                     (reinterpret_cast<uintptr_t>(y) & 15) == 0 && std::getenv("CB_TMA_TSTORE");
     prm.bulk_parts = std::getenv("CB_TMA_BULK_PARTS") ? 1 : 0;
+    prm.out_al16 = (reinterpret_cast<uintptr_t>(y) & 15) == 0 ? 1 : 0;
+    prm.range_kb = std::max(1, promote_k(bf16) / (128 / L.eb));
     if (std::getenv("CB_TMA_TRACE")) prm.trace = debug_trace_buffer(pl.grid, st);
     if (pl.splits > 1) {
         int rc = launch_fill_bias(g.N, g.K, g.PQ, bias, y, st);

@@ -136,3 +136,66 @@ def test_install_into_reference_shaped_harness():
         ref.conv_main_blocked_direct(grouped, None)
     undo()
     assert (ref.conv_main_blocked_direct, ref.PhaseLedger) == ("m", "L")
+
+
+def test_install_into_the_real_reference_harness(tmp_path):
+    """install() against the unmodified reference convbench.harness: globals rebound, an
+    unsupported descriptor goes through the reference run_single as skipped_unsupported
+    (before any device work), the parity allclose replaces the reference's, undo restores."""
+    from refpkg import reference
+    cb = reference()
+    if cb is None:
+        pytest.skip("reference convbench not installed (baseline/_ref)")
+    ref_h = cb.harness
+    before = {n: getattr(ref_h, n) for n in ("conv_main_blocked_direct", "conv_baseline_im2col_gemm",
+                                             "PhaseLedger", "allclose")}
+    undo = install(ref_h)
+    try:
+        from paper_2407_10730_b200 import algos
+        assert algos._INPUT_CACHE_ON
+        desc = cb.descriptor.ConvDescriptor(batch=1, in_channels=4, in_h=6, in_w=6,
+                                            out_channels=4, k_h=3, k_w=3, groups=2)
+        out = ref_h.run_single(desc, cb.harness.RunConfig(mode="main", warmups=0, runs=1))
+        assert out.status == "skipped_unsupported", out
+        # the parity allclose: max|a-b| / sqrt(C/g*R*S) of the op the wrappers saw last
+        a = np.zeros((1, 4, 4, 4), np.float32)
+        b = a.copy()
+        b[0, 0, 0, 0] = 6e-4 * np.sqrt(2 * 9)
+        ok, err = ref_h.allclose(a, b)
+        assert not ok and abs(err - 6e-4) < 1e-9
+    finally:
+        undo()
+    assert {n: getattr(ref_h, n) for n in before} == before
+    from paper_2407_10730_b200 import algos
+    assert not algos._INPUT_CACHE_ON
+
+
+def test_reference_report_reads_our_results_csv(tmp_path):
+    """`convbench report` (the unmodified reference CLI, report.py:21-34,149-184) joins
+    results CSVs written by this package's writer into its speedup / breakdown outputs."""
+    from refpkg import reference
+    cb = reference()
+    if cb is None:
+        pytest.skip("reference convbench not installed (baseline/_ref)")
+    from paper_2407_10730_b200 import report
+    from paper_2407_10730_b200.harness import RunOutcome
+    from paper_2407_10730_b200.timing import _report, aggregate
+    rows = {}
+    for mode, scale in (("main", 1), ("baseline", 3)):
+        recs = []
+        for i, d in enumerate((D(), D(in_channels=8, out_channels=16), D(k_h=1, k_w=1))):
+            st = aggregate([_report([0, 10 * scale, 5, 20 * scale, 400 * scale + i, 7, 0],
+                                    [1, 1, 1, 1, 1, 1, 0])])
+            recs.append(report.outcome_record(RunOutcome(key=key_of(d), mode=mode, runs=1,
+                                                         warmups=0, status="ok", stats=st)))
+        rows[mode] = tmp_path / f"results_{mode}.csv"
+        report.write_results_csv(recs, rows[mode])
+    outs = {k: tmp_path / f"{k}.csv" for k in ("speedup", "breakdown")}
+    summary = tmp_path / "summary.json"
+    rc = cb.cli.main(["report", "--main", str(rows["main"]), "--baseline", str(rows["baseline"]),
+                      "--out-speedup", str(outs["speedup"]), "--out-breakdown",
+                      str(outs["breakdown"]), "--out-summary", str(summary)])
+    assert rc in (0, None)
+    sp = outs["speedup"].read_text().splitlines()
+    assert len(sp) == 4, sp  # header + 3 ops
+    assert summary.exists() and outs["breakdown"].exists()

@@ -121,7 +121,7 @@ def test_sconv_matches_oracle_on_supported(cuda, variant):
 
 def test_im2col_bit_exact(cuda):
     from paper_2407_10730_b200.algos import im2col_transform
-    for d in SMALL + [cfg("cfg1"), cfg("cfg2a"), cfg("cfg2b"), cfg("cfg3", batch=2)]:
+    for d in SMALL + [cfg("cfg1"), cfg("cfg2a"), cfg("cfg2b"), cfg("cfg3"), cfg("cfg4")]:
         inp, (x, _, _) = _inputs(d)
         got = im2col_transform(inp)
         want = orc.im2col(d, x)
@@ -378,3 +378,62 @@ def test_activation_split_variants_agree(cuda, monkeypatch):
     _check_conv(d, y_wide, orc.conv_direct_naive(d, x, w, b))
     monkeypatch.setenv("CB_K0_NARROW", "1")
     assert np.array_equal(conv_fused(inp, variant="tc3xbf16"), y_wide)
+
+
+def _sweep_classes(max_flops: float, per_class: int) -> dict:
+    """Config-5 sweep ops grouped by the fused path / plan the planner picks for them
+    (ffma, gather, K7 direct, stacked taps, folded taps, K parts > 4 per tile, tail split,
+    plain TMA tiles): the cheapest `per_class` and the largest `per_class` ops of each class
+    under `max_flops`."""
+    from paper_2407_10730_b200 import algos, configs
+    from paper_2407_10730_b200.descriptor import flop_count
+    out: dict = {}
+    for d in sorted(set(configs.sweep()), key=lambda d: (flop_count(d), str(d))):
+        if flop_count(d) > max_flops:
+            continue
+        v = algos.resolve_variant(d, "auto")
+        if v == "ffma":
+            out.setdefault("ffma", []).append(d)
+            continue
+        lay = algos.fused_layout(d, v)
+        if lay["path"] != 1:
+            out.setdefault(f"path{lay['path']}", []).append(d)
+            continue
+        plan = algos.fused_plan(d, v)
+        tiles = plan["m_tiles"] * plan["n_tiles"]
+        if lay["weight_rows"] != d.out_channels:
+            out.setdefault("stacked", []).append(d)
+        elif d.k_w > 1 and lay["chunk_channels"] >= d.in_channels * d.k_w:
+            out.setdefault("folded", []).append(d)
+        key = "parts>4" if plan["ctas"] > 4 * tiles else "split" if plan["ctas"] > tiles else "plain"
+        out.setdefault(key, []).append(d)
+    picked = {k: v[:per_class] + v[per_class:][-per_class:] for k, v in out.items()}
+    # the many-part tail split of the widest reductions (C=2048, 5x5 / 7x7)
+    wide = [d for d in out.get("parts>4", []) if d.in_channels == 2048 and d.k_h in (5, 7)]
+    picked["parts>4"] += [d for d in wide[::max(1, len(wide) // per_class)] if d not in picked["parts>4"]]
+    return picked
+
+
+def test_sweep_plan_classes_match_oracle(cuda):
+    """Config-5 ops from every planner class -- including the many-K-part tail split of
+    C=2048 5x5 / 7x7 reductions, tap stacking, tap folding and K7 -- through the fused
+    (auto), Im2col-GEMM and SConv paths, against the float64 oracle on make_inputs data.
+    (tests/sweep_parity.py runs the same check on all 9243 ops.)"""
+    from paper_2407_10730_b200.algos import (conv_baseline_im2col_gemm, conv_fused,
+                                             conv_main_blocked_direct)
+    from paper_2407_10730_b200.timing import PhaseLedger
+    classes = _sweep_classes(3e9, 3)
+    for want in ("ffma", "path2", "stacked", "folded", "parts>4", "split", "plain"):
+        assert len(classes.get(want, [])) >= 2, (want, sorted(classes))
+    assert any(d.in_channels == 2048 and d.k_h in (5, 7) for d in classes["parts>4"])
+    worst = {}
+    for name, ds in classes.items():
+        for d in ds:
+            inp, (x, w, b) = _inputs(d)
+            ref = orc.conv_banded64(d, x, w, b).astype(np.float32)
+            for path, fn in (("fused", lambda: conv_fused(inp)),
+                             ("im2col", lambda: conv_baseline_im2col_gemm(inp, PhaseLedger())),
+                             ("sconv", lambda: conv_main_blocked_direct(inp, PhaseLedger()))):
+                e = _check_conv(d, fn(), ref)
+                worst[(name, path)] = max(worst.get((name, path), 0.0), e)
+    print({f"{k[0]}/{k[1]}": f"{v:.1e}" for k, v in sorted(worst.items())})

@@ -60,6 +60,10 @@ def test_corpus_oracle_outputs(corpus):
         # the float64 im2col GEMM oracle agrees to fp32 rounding
         assert orc.normalized_max_err(orc.conv_im2col64(d, x, w, b), want,
                                       orc.reduction_len(d)) < 1e-6
+        # the banded float64 oracle of the sweep parity run, with bands of 1-2 rows
+        for cap in (1, 1 << 12):
+            got64 = orc.conv_banded64(d, x, w, b, max_cols_bytes=cap)
+            assert orc.normalized_max_err(got64, want, orc.reduction_len(d)) < 1e-6, r["key"]
         if i < 6:  # literal loops on the smallest shapes (reference tests/oracles.py:43-80)
             assert orc.normalized_max_err(orc.conv_loops(d, x, w, b), want,
                                           orc.reduction_len(d)) < 1e-6
