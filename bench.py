@@ -34,8 +34,9 @@ Keys of the JSON line (rank 0):
                dense bf16 is a secondary field.
 * variants     the same workload with the north_star's 3xTF32 split (and 3xBF16).
 * configs      configs 1-4 x {fused, Im2col-GEMM, SConv}: graph-replayed phase times with an
-               L2 flush before every replay, GFLOP/s, roofline fractions of the fused kernel
-               and of the packing kernels (K1 / K2 GB/s vs the HBM peak).
+               L2 flush before every replay (write 256 MB, then read 256 MB so the flush
+               leaves no dirty lines), GFLOP/s, roofline fractions of the fused kernel and
+               of the packing kernels (K1 / K2 GB/s vs the HBM peak).
 * cpu_baseline the reference CPU algorithms (the unmodified reference from baseline/_ref,
                else the oracle port), rank 0 at N=1: 1 thread and all threads, both
                algorithms, configs 1-4 on bounded samples; the headline value is SConv
@@ -407,7 +408,15 @@ def config_table(peaks, runs: int = 5):
     from paper_2407_10730_b200.harness import RunConfig, make_inputs, to_device
     from paper_2407_10730_b200.roofline import conv_roofline
     from paper_2407_10730_b200.timing import EventLedger, Phase, aggregate
-    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > 2x L2
+    # L2 flush between replays: write 256 MB (> 2x L2), then read another 256 MB so the
+    # written lines are evicted clean before the replay (the write-back of dirty flush lines
+    # would otherwise land inside the next op's first phase)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    flush_rd = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        flush.zero_()
+        flush_rd.sum()
     hbm = peaks["hbm_gbs"] * 1e9
     table, samples = {}, {}
     for name in TABLE_CONFIGS:
@@ -433,7 +442,7 @@ def config_table(peaks, runs: int = 5):
                 y = fn(inp, led)
             reps = []
             for r in range(runs + 1):
-                flush.zero_()
+                flush_l2()
                 graph.replay()
                 if r >= 1:
                     reps.append(led.snapshot())
@@ -467,7 +476,7 @@ def config_table(peaks, runs: int = 5):
         table[name] = row
         del inp
         torch.cuda.empty_cache()
-    del flush
+    del flush, flush_rd
     return table, samples
 
 

@@ -256,6 +256,10 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             for (int rg = 0; rg < nranges; ++rg, ++i) {
             ptx::mbar_wait(acc_full, i & 1);
             ptx::tc_fence_after();
+            if (ncol <= 0) {  // no valid channel in this item: release the accumulator anyway
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(acc_empty);
+            }
             const bool add = p.add_mode || rg > 0;  // later ranges add to the first's store
 #pragma unroll 1
             for (int c0 = 0; c0 < ncol; c0 += 32) {
@@ -270,10 +274,13 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 const int nvalid = min(32, ncol - c0);
                 const int fb = gi * g.kpg + f_tile0 + c0;
                 float* dst = p.out + obase + (int64_t)fb * ostride;
-                if (add) {
+                if (add) {  // all loads before the first store (no per-element round trips)
+                    float o[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] = e < nvalid ? __ldcg(dst + (int64_t)e * ostride) : 0.f;
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
-                        if (e < nvalid) dst[(int64_t)e * ostride] += __uint_as_float(r[e]);
+                        if (e < nvalid) dst[(int64_t)e * ostride] = __uint_as_float(r[e]) + o[e];
                 } else {
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
@@ -520,7 +527,10 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
         const int64_t tail = prm.items % grid;
         static const bool no_split = std::getenv("CB_K8_NO_TAIL_SPLIT") != nullptr;
         if (!no_split && prm.items > grid && tail > 0) {
-            const int parts = (int)std::min<int64_t>(std::min<int64_t>(grid / tail, 4), bn / 32);
+            // parts of 32+ channels that hold real output channels (a part past kpg would
+            // have nothing to store)
+            const int parts = (int)std::min<int64_t>(std::min<int64_t>(grid / tail, 4),
+                                                     (std::min(bn, g.kpg) + 31) / 32);
             if (parts >= 2) {
                 prm.full_items = prm.items - tail;
                 prm.tail_split = parts;

@@ -43,7 +43,7 @@ struct TsParams {
     int kp;             // reduction padded to 32 (A columns per half: kp / 2)
     int n_pad;          // output channels padded to 16 (MMA N)
     int kb_w;           // split weight row length (multiple of 64)
-    int tiles_per_img;  // ceil(PQ / 128)
+    int tiles_per_img;  // ceil(PQ / (128 * CG)): tiles of one CTA (CG = 1) or pair (CG = 2)
     int64_t total_tiles;
     int box_rows, box_w;    // staging window: input rows x padded row width
     int x0;                 // window column 0 = input column -x0 (x0 = pw rounded up to 4)
@@ -52,7 +52,8 @@ struct TsParams {
     int nwin;               // staging windows in the ring (2..4): the window TMA of tile i +
                             // nwin - 1 is in flight while tile i is built (its L2 latency,
                             // ~2.6k cycles on cfg3, exceeds one tile's A build)
-    uint32_t w_half_bytes;  // n_pad * kb_w * 2
+    uint32_t w_half_bytes;  // (n_pad / CG) * kb_w * 2: this CTA's weight rows, one half
+    int w_rows;             // n_pad / CG
     int debug;              // diagnostics (CB_TS_DEBUG): 1 no MMA, 2 no tcgen05.st, 4 no input TMA
     int tma_store;          // 1: epilogue stages 32-channel chunks in smem, TMA stores them
     float inv_q;            // 1 / Q (pixel -> output row without an integer division)
@@ -69,8 +70,8 @@ struct TsParams {
 // Persistent tile walk without 64-bit divisions: tile t = n * tiles_per_img + ti, advanced
 // by gridDim.x = step_n * tiles_per_img + step_ti.
 struct TileWalk {
-    int t, n, ti, step_n, step_ti;
-    __device__ __forceinline__ explicit TileWalk(const struct TsParams& p);
+    int t, n, ti, step_n, step_ti, units;
+    __device__ __forceinline__ TileWalk(const struct TsParams& p, int unit, int nunits);
     __device__ __forceinline__ void next(const struct TsParams& p);
 };
 
@@ -79,15 +80,16 @@ __device__ __forceinline__ void ts_stamp(const TsParams& p, int e, int i) {
     if (p.trace && blockIdx.x < 4 && i < 512) p.trace[blockIdx.x * 8192 + e * 512 + i] = clock64();
 }
 
-__device__ __forceinline__ TileWalk::TileWalk(const TsParams& p) {
-    t = blockIdx.x;
+__device__ __forceinline__ TileWalk::TileWalk(const TsParams& p, int unit, int nunits) {
+    t = unit;
+    units = nunits;
     n = t / p.tiles_per_img;
     ti = t - n * p.tiles_per_img;
-    step_n = gridDim.x / p.tiles_per_img;
-    step_ti = gridDim.x - step_n * p.tiles_per_img;
+    step_n = nunits / p.tiles_per_img;
+    step_ti = nunits - step_n * p.tiles_per_img;
 }
 __device__ __forceinline__ void TileWalk::next(const TsParams& p) {
-    t += gridDim.x;
+    t += units;
     n += step_n;
     ti += step_ti;
     if (ti >= p.tiles_per_img) {
@@ -254,6 +256,7 @@ __device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_
 // compile-time reduction layouts (TsParams::fixed): 0 = generic offset-table producer
 #define CB_TS_FIXED_LIST(X) X(1, 3, 7, 7) X(2, 3, 3, 3) X(3, 3, 5, 5) X(4, 4, 3, 3) X(5, 4, 7, 7)
 
+template <int CG>
 __global__ void __launch_bounds__(TS_THREADS, 1)
 conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUtensorMap tm_x,
                const __grid_constant__ CUtensorMap tm_whi, const __grid_constant__ CUtensorMap tm_wlo,
@@ -279,6 +282,11 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const Geom& g = p.g;
+    // CTA pair (CG = 2): each CTA stages its own window, builds its own 128 pixel rows of A
+    // in its own TMEM and holds half of the weight rows; the leader (rank 0) issues M = 256
+    // MMAs over both, and the commits multicast to both CTAs' barriers.
+    const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
+    const int unit0 = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;
     const int col_a0 = 2 * p.n_pad;  // TMEM: [acc0 | acc1 | A0 (hi, lo) | A1 (hi, lo)]
     const int half_cols = p.kp / 2;
 
@@ -289,10 +297,10 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             ptx::mbar_init(&s_empty[b], 32 * TS_PROD_WARPS);
         }
         for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&a_full[b], 32 * TS_PROD_WARPS);
+            ptx::mbar_init(&a_full[b], CG * 32 * TS_PROD_WARPS);
             ptx::mbar_init(&a_empty[b], 1);
             ptx::mbar_init(&acc_full[b], 1);
-            ptx::mbar_init(&acc_empty[b], 128);
+            ptx::mbar_init(&acc_empty[b], CG * 128);
         }
         ptx::fence_mbar_init();
     }
@@ -301,10 +309,21 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         ptx::tma_prefetch_desc(&tm_whi);
         ptx::tma_prefetch_desc(&tm_wlo);
     }
-    if (warp == TS_MMA_WARP) ptx::tmem_alloc(tmem_slot, TS_TMEM_COLS);
+    if (warp == TS_MMA_WARP) {
+        if (CG == 2)
+            ptx::tmem_alloc_pair(tmem_slot, TS_TMEM_COLS);
+        else
+            ptx::tmem_alloc(tmem_slot, TS_TMEM_COLS);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (CG == 2)
+        ptx::cluster_sync();
+    else
+        __syncthreads();
     ptx::tc_fence_after();
+    // the leader's barriers, addressed from either CTA of a pair
+    const uint32_t a_full_l0 = CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&a_full[0]), 0) : 0;
+    const uint32_t acc_empty_l0 = CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), 0) : 0;
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) ts_stamp(p, 15, 0);
 
@@ -334,11 +353,13 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         int i = 0;
         int ws = 0;  // staging-window ring slot and phase
         uint32_t wph = 0;
-        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
+        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const int n = tw.n;
-            const int p0 = tw.ti * TS_BM;
+            // this CTA's first pixel; past the image (the second half of a pair's last tile)
+            // the window origin stays inside it and nothing is stored
+            const int p0 = min(tw.ti * (TS_BM * CG) + (int)rank * TS_BM, g.PQ - 1);
             const int oy_a = div_q(p0, p);
             const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
             const int oy = div_q(pix, p);
@@ -406,7 +427,10 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 4 : 14, i);
-            ptx::mbar_arrive(&a_full[b]);
+            if (CG == 2)
+                ptx::mbar_arrive_remote(a_full_l0 + b * sizeof(uint64_t));
+            else
+                ptx::mbar_arrive(&a_full[b]);
             ptx::mbar_arrive(&s_empty[ws]);
             if (++ws == p.nwin) {
                 ws = 0;
@@ -422,11 +446,11 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         const int m = quad * 32 + lane;
         const bool issuer = threadIdx.x == TS_EPI_WARP0 * 32;
         int i = 0, chunk = 0;
-        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
+        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const int n = tw.n;
-            const int p0 = tw.ti * TS_BM;
+            const int p0 = tw.ti * (TS_BM * CG) + (int)rank * TS_BM;
             const int pix = p0 + m;
             const bool valid = pix < g.PQ;
             float* dst = p.out + (int64_t)n * g.K * g.PQ + pix;
@@ -441,7 +465,10 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 ptx::tmem_ld_wait();
                 if (c0 + 32 >= g.K) {  // accumulator fully in registers: release it early
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(&acc_empty[b]);
+                    if (CG == 2)
+                        ptx::mbar_arrive_remote(acc_empty_l0 + b * sizeof(uint64_t));
+                    else
+                        ptx::mbar_arrive(&acc_empty[b]);
                     if (threadIdx.x == TS_EPI_WARP0 * 32) ts_stamp(p, 8, i);
                 }
                 if (p.debug & 8) continue;
@@ -461,7 +488,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                     }
                     ptx::fence_proxy_async_smem();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (issuer) {
+                    if (issuer && p0 < g.PQ) {
                         ptx::tma_store_3d(&tm_y, buf, p0, c0, n);
                         ptx::bulk_commit();
                         ts_stamp(p, 9, i);
@@ -482,22 +509,28 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         // ============================ TMA: weights once, then input windows =============
         const uint32_t leader = ptx::elect_one();
         const int wblocks = p.kb_w / 64;
-        if (leader) {
-            ptx::mbar_arrive_expect_tx(w_full, 2 * p.w_half_bytes);
+        if (leader) {  // this CTA's weight rows [rank * w_rows, +w_rows); pairs: leader barrier
+            if (rank == 0) ptx::mbar_arrive_expect_tx(w_full, CG * 2 * p.w_half_bytes);
+            const int row0 = (int)rank * p.w_rows;
             for (int kb = 0; kb < wblocks; ++kb) {
-                ptx::tma_load_2d(w_hi + (size_t)kb * p.n_pad * 128, &tm_whi, w_full, kb * 64, 0);
-                ptx::tma_load_2d(w_lo + (size_t)kb * p.n_pad * 128, &tm_wlo, w_full, kb * 64, 0);
+                uint8_t* dh = w_hi + (size_t)kb * p.w_rows * 128;
+                uint8_t* dl = w_lo + (size_t)kb * p.w_rows * 128;
+                if (CG == 2) {
+                    ptx::tma_load_2d_pair(dh, &tm_whi, ptx::leader_bar(w_full), kb * 64, row0);
+                    ptx::tma_load_2d_pair(dl, &tm_wlo, ptx::leader_bar(w_full), kb * 64, row0);
+                } else {
+                    ptx::tma_load_2d(dh, &tm_whi, w_full, kb * 64, row0);
+                    ptx::tma_load_2d(dl, &tm_wlo, w_full, kb * 64, row0);
+                }
             }
         }
         __syncwarp();
         int i = 0;
         int ws = 0;  // staging-window ring slot and phase
         uint32_t wph = 0;
-        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
-            const int b = i & 1;
-            const uint32_t ph = (i >> 1) & 1;
+        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
             const int n = tw.n;
-            const int p0 = tw.ti * TS_BM;
+            const int p0 = min(tw.ti * (TS_BM * CG) + (int)rank * TS_BM, g.PQ - 1);
             const int iy0 = div_q(p0, p) * g.sh - g.ph;
             ptx::mbar_wait(&s_empty[ws], wph ^ 1);
             if (leader) ts_stamp(p, 0, i);
@@ -517,14 +550,14 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     } else {
         // ============================ MMA issuer ========================================
         const uint32_t leader = ptx::elect_one();
-        const uint32_t idesc = ptx::idesc_f32acc<true>(TS_BM, p.n_pad);
+        const uint32_t idesc = ptx::idesc_f32acc<true>(TS_BM * CG, p.n_pad);
         const uint64_t dbh0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_hi));
         const uint64_t dbl0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_lo));
-        const uint32_t blk16 = (uint32_t)(p.n_pad * 128) >> 4;  // one 64-wide K block of B
+        const uint32_t blk16 = (uint32_t)(p.w_rows * 128) >> 4;  // one 64-wide K block of B
         const int ksteps = p.kp / 16;
-        ptx::mbar_wait(w_full, 0);
+        if (rank == 0) ptx::mbar_wait(w_full, 0);
         int i = 0;
-        for (TileWalk tw(p); tw.t < p.total_tiles; tw.next(p), ++i) {
+        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles && rank == 0; tw.next(p), ++i) {
             const int b = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             ptx::mbar_wait(&a_full[b], ph);
@@ -538,12 +571,23 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             if (leader) {
                 for (int j = 0; j < ksteps && !(p.debug & 1); ++j) {
                     const uint64_t boff = (uint64_t)((j >> 2) * blk16 + (j & 3) * 2);
-                    ptx::umma_ts_bf16(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
-                    ptx::umma_ts_bf16(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
-                    ptx::umma_ts_bf16(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
+                    if (CG == 2) {
+                        ptx::umma_ts_bf16_pair(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
+                        ptx::umma_ts_bf16_pair(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
+                        ptx::umma_ts_bf16_pair(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
+                    } else {
+                        ptx::umma_ts_bf16(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
+                        ptx::umma_ts_bf16(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
+                        ptx::umma_ts_bf16(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
+                    }
                 }
-                ptx::umma_commit(&a_empty[b]);
-                ptx::umma_commit(&acc_full[b]);
+                if (CG == 2) {
+                    ptx::umma_commit_pair(&a_empty[b]);
+                    ptx::umma_commit_pair(&acc_full[b]);
+                } else {
+                    ptx::umma_commit(&a_empty[b]);
+                    ptx::umma_commit(&acc_full[b]);
+                }
                 ts_stamp(p, 10, i);
             }
             __syncwarp();
@@ -551,10 +595,16 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if (CG == 2)
+        ptx::cluster_sync();
+    else
+        __syncthreads();
     if (warp == TS_MMA_WARP) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TS_TMEM_COLS);
+        if (CG == 2)
+            ptx::tmem_dealloc_pair(tmem_base, TS_TMEM_COLS);
+        else
+            ptx::tmem_dealloc(tmem_base, TS_TMEM_COLS);
     }
 }
 
@@ -563,6 +613,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
 // ----------------------------------------------------------------------------------------
 struct TsPlan {
     bool ok;
+    int cg;  // 1: one CTA per 128-pixel tile; 2: CTA pairs (cta_group::2) on 256-pixel tiles
     int kp, n_pad, kb_w, box_rows, box_w, x0, pair, pf, kdim;
     uint32_t stage_bytes, stage_stride, w_half_bytes;
     int nwin;
@@ -607,7 +658,15 @@ static TsPlan plan_ts(const Geom& g) {
     if (pl.box_w > 256 || pl.box_rows > 256 || g.C > 256 || (g.W % 4) != 0) return pl;
     pl.stage_bytes = (uint32_t)g.C * pl.box_rows * pl.box_w * 4;
     pl.stage_stride = (pl.stage_bytes + 1023) / 1024 * 1024;
-    pl.w_half_bytes = (uint32_t)pl.n_pad * pl.kb_w * 2;
+    // CTA pairs halve each SM's weight reads (the B operand, ~30% of the shared-memory
+    // traffic of a tile): N split N/2 per CTA, needs N/2 a multiple of 16 (SW128 atoms)
+    pl.cg = 1;
+    {
+        const char* e = std::getenv("CB_TS_CG");
+        const int want = e ? std::atoi(e) : 1;  // pairs measured slower on cfg3 (30 vs 22 us)
+        if (want == 2 && pl.n_pad % 32 == 0 && pl.n_pad <= 256) pl.cg = 2;
+    }
+    pl.w_half_bytes = (uint32_t)(pl.n_pad / pl.cg) * pl.kb_w * 2;
     // >= 120 KB keeps one CTA per SM (each allocates all 512 TMEM columns)
     pl.tma_store = (g.PQ % 4) == 0;  // 16-byte global strides for the output map
     auto smem_for = [&](int nwin) {
@@ -641,9 +700,9 @@ int ts_weight_kdim(const Geom& g, int* pair, int* pf) {
 int ts_plan_query(const Geom& g, cb_tile_plan* out) {
     const TsPlan pl = plan_ts(g);
     if (!pl.ok) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
-    const int64_t tiles = (int64_t)g.N * ((g.PQ + TS_BM - 1) / TS_BM);
+    const int64_t tiles = (int64_t)g.N * ((g.PQ + TS_BM * pl.cg - 1) / (TS_BM * pl.cg));
     out->variant = CB_VARIANT_TC3XBF16;
-    out->block_m = TS_BM;
+    out->block_m = TS_BM * pl.cg;
     out->block_n = pl.n_pad;
     out->block_k = 16;
     out->stages = 2;
@@ -651,7 +710,7 @@ int ts_plan_query(const Geom& g, cb_tile_plan* out) {
     out->m_tiles = tiles;
     out->n_tiles = 1;
     out->k_blocks = pl.kp / 16;
-    out->ctas = (int)std::min<int64_t>(tiles, sm_count());
+    out->ctas = (int)std::min<int64_t>(tiles, sm_count() / pl.cg) * pl.cg;
     return CB_OK;
 }
 
@@ -695,7 +754,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     for (int h = 0; h < 2; ++h) {
         cuuint64_t dims[2] = {(cuuint64_t)pl.kb_w, (cuuint64_t)g.K};
         cuuint64_t strides[1] = {(cuuint64_t)pl.kb_w * 2};
-        cuuint32_t box[2] = {64, (cuuint32_t)pl.n_pad};
+        cuuint32_t box[2] = {64, (cuuint32_t)(pl.n_pad / pl.cg)};
         cuuint32_t es[2] = {1, 1};
         CUresult r = enc(h ? &mwl : &mwh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                          const_cast<void*>(h ? w_lo : w_hi), dims, strides, box, es,
@@ -726,7 +785,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.kp = pl.kp;
     prm.n_pad = pl.n_pad;
     prm.kb_w = pl.kb_w;
-    prm.tiles_per_img = (g.PQ + TS_BM - 1) / TS_BM;
+    prm.tiles_per_img = (g.PQ + TS_BM * pl.cg - 1) / (TS_BM * pl.cg);
     prm.inv_q = 1.0f / (float)g.Q;
     prm.fixed = ts_fixed_id(g);
     prm.pair = pl.pair;
@@ -739,18 +798,36 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.stage_stride = pl.stage_stride;
     prm.nwin = pl.nwin;
     prm.w_half_bytes = pl.w_half_bytes;
+    prm.w_rows = pl.n_pad / pl.cg;
     if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
     if (std::getenv("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(conv_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        attr_err = cudaFuncSetAttribute(conv_ts_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(conv_ts_kernel<2>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
     if (attr_err != cudaSuccess)
         return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-    const int grid = (int)std::min<int64_t>(prm.total_tiles, sm_count());
-    conv_ts_kernel<<<grid, TS_THREADS, pl.smem, st>>>(prm, mx, mwh, mwl, my);
+    const int units = (int)std::min<int64_t>(prm.total_tiles, sm_count() / pl.cg);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(units * pl.cg));
+    cfg.blockDim = dim3(TS_THREADS);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.cg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pl.cg == 2 ? 1 : 0;  // no cluster attribute for single CTAs
+    cudaError_t e = pl.cg == 2 ? cudaLaunchKernelEx(&cfg, conv_ts_kernel<2>, prm, mx, mwh, mwl, my)
+                               : cudaLaunchKernelEx(&cfg, conv_ts_kernel<1>, prm, mx, mwh, mwl, my);
+    if (e != cudaSuccess) return fail(CB_ERR_CUDA, std::string("conv_ts launch: ") + cudaGetErrorString(e));
     return check_launch("conv_ts_kernel");
 }
 

@@ -559,10 +559,45 @@ unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int6
     }
 }
 
+// K5 when every slice is a whole image (band_rows >= P): the chunk's accumulators
+// [image][channel][pixel] have exactly y's NCHW layout, so the unpack is a flat copy of the
+// chunk's images with the channel bias added.  float4 lanes, 4 vectors in flight per thread.
+__global__ void __launch_bounds__(256)
+unpack_images_kernel(int64_t nvec, int pq4, int K, const float4* __restrict__ acc,
+                     const float* __restrict__ bias, float4* __restrict__ y) {
+    const int64_t stride = (int64_t)gridDim.x * 256;
+    for (int64_t v0 = blockIdx.x * 256LL + threadIdx.x; v0 < nvec; v0 += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (v0 + u * stride < nvec) v[u] = __ldcs(acc + v0 + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = v0 + u * stride;
+            if (i >= nvec) break;
+            if (bias) {
+                const float b = __ldg(bias + (int)((i / pq4) % K));
+                v[u].x += b, v[u].y += b, v[u].z += b, v[u].w += b;
+            }
+            y[i] = v[u];
+        }
+    }
+}
+
 int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count,
                   const float* acc, const float* bias, float* y, cudaStream_t st) {
     const int64_t total = j_count * g.K;
     if (total == 0) return CB_OK;
+    if (band_rows >= g.P && g.PQ % 4 == 0 && j_begin % g.PQ == 0 && j_count % g.PQ == 0 &&
+        ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(y)) & 15) == 0 &&
+        !std::getenv("CB_K5_ROWS")) {
+        const int64_t nvec = total / 4;
+        const int64_t blocks = std::min<int64_t>((nvec + 1023) / 1024, (int64_t)sm_count() * 8);
+        unpack_images_kernel<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, st>>>(
+            nvec, g.PQ / 4, g.K, reinterpret_cast<const float4*>(acc), bias,
+            reinterpret_cast<float4*>(y + (j_begin / g.PQ) * (int64_t)g.K * g.PQ));
+        return check_launch("unpack_images");
+    }
     // the launch covers whole slices: count them from the first slice's index
     const int per_img = (g.P + band_rows - 1) / band_rows;
     const int64_t n0 = j_begin / g.PQ;

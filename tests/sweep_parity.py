@@ -58,31 +58,58 @@ def _worker_init(root: str) -> None:
     threadpool_limits(1)  # one core per worker: the pool is the parallelism
 
 
-def _check_job(desc, data_seed: int, items: list) -> list:
-    """Oracle of one op key, compared with every output of that key."""
+def oracle_channels(desc, max_flops: float) -> np.ndarray | None:
+    """Output channels the oracle computes for one op: all of them (None) up to max_flops of
+    oracle work, else a seeded subset of ceil(K * max_flops / flops) >= 8 channels (every
+    pixel of each), so the sweep's largest ops (up to 2e13 FLOPs) are checked too."""
+    from paper_2407_10730_b200.descriptor import flop_count, key_of
+    f = flop_count(desc)
+    if f <= max_flops or desc.groups != 1:
+        return None
+    k = min(desc.out_channels, max(8, math.ceil(desc.out_channels * max_flops / f)))
+    rng = np.random.default_rng(int.from_bytes(key_of(desc).encode()[-8:], "little"))
+    return np.sort(rng.choice(desc.out_channels, size=k, replace=False))
+
+
+def _check_job(desc, data_seed: int, items: list, channels=None) -> list:
+    """Oracle of one op key (all output channels, or `channels`), compared with every output
+    of that key."""
+    from dataclasses import replace
     from oracle import conv_oracle as orc
     t0 = time.perf_counter()
     x, w, b = orc.make_inputs(desc, data_seed)
-    ref64 = orc.conv_banded64(desc, x, w, b)
+    if channels is not None:  # the same conv restricted to a subset of output channels
+        d_sub = replace(desc, out_channels=len(channels))
+        ref64 = orc.conv_banded64(d_sub, x, np.ascontiguousarray(w[channels]),
+                                  None if b is None else b[channels])
+    else:
+        ref64 = orc.conv_banded64(desc, x, w, b)
     want = ref64.astype(np.float32)  # conv_direct_naive's output: one final fp32 rounding
     red = orc.reduction_len(desc)
     t_ref = time.perf_counter() - t0
+    note0 = None if channels is None else f"{len(channels)}/{desc.out_channels} channels"
     res = []
     for index, mode, path in items:
-        y = np.load(path)
+        y = np.load(path, mmap_mode="r")
+        if channels is not None and y.ndim == 4:
+            y = y[:, channels]
+        y = np.ascontiguousarray(y)
         os.unlink(path)
         if y.shape != want.shape:
             res.append((index, mode, math.inf, math.inf, f"shape {y.shape} != {want.shape}"))
             continue
         err = orc.normalized_max_err(y, want, red)
         rel = orc.reference_allclose_err(y, want)
-        res.append((index, mode, err, rel, None))
+        res.append((index, mode, err, rel, note0))
     return [(i, m, e, r, note, t_ref) for i, m, e, r, note in res]
 
 
 class OracleChecker:
-    def __init__(self, data_seed: int, workers: int, pending: int, spool: str | None = None):
+    def __init__(self, data_seed: int, workers: int, pending: int, spool: str | None = None,
+                 journal: str | None = None, max_oracle_flops: float = 3e10):
         import multiprocessing as mp
+        self.max_oracle_flops = max_oracle_flops
+        self.journal = open(journal, "a") if journal else None  # results as they arrive
         self.data_seed = data_seed
         self.workers = workers
         self.pending_max = pending
@@ -93,14 +120,25 @@ class OracleChecker:
         self.futures = []
         self.results: dict[str, dict] = {}
         self.oracle_s = 0.0
+        self.blocked_s = 0.0
         self.keys = 0
 
+    def progress(self) -> str:
+        return (f"(oracle: {len(self.results)} outputs checked, {len(self.futures)} keys pending, "
+                f"{self.blocked_s:.0f} s blocked on the pool)")
+
     def _drain(self, keep: int) -> None:
+        t0 = time.perf_counter()
         while len(self.futures) > keep:
             f = self.futures.pop(0)
             for i, m, e, r, note, t_ref in f.result():
                 self.results[f"{i}:{m}"] = {"err": e, "allclose_rel_err": r, "note": note}
+                if self.journal:
+                    self.journal.write(f"{i},{m},{e:.4e},{r:.4e},{note or ''}\n")
+            if self.journal:
+                self.journal.flush()
             self.oracle_s += t_ref
+        self.blocked_s += time.perf_counter() - t0
 
     def check(self, desc, host, outs) -> None:
         items = []
@@ -110,7 +148,8 @@ class OracleChecker:
             items.append((i, m, path))
         if not items:
             return
-        self.futures.append(self.pool.submit(_check_job, desc, self.data_seed, items))
+        self.futures.append(self.pool.submit(_check_job, desc, self.data_seed, items,
+                                             oracle_channels(desc, self.max_oracle_flops)))
         self.keys += 1
         self._drain(self.pending_max)
 
@@ -155,6 +194,9 @@ class OracleChecker:
                           "conv_direct_naive's sums, algos.py:212-240), rounded once to fp32",
                 "inputs": "oracle/conv_oracle.make_inputs (bit-identical to harness.py:79-96)",
                 "workers_per_rank": self.workers, "host_cpu": cpu, "cpu_count": os.cpu_count(),
+                "coverage": f"every output of ops up to {self.max_oracle_flops / 1e9:g} GFLOP; "
+                            "larger ops: every pixel of a seeded subset of ceil(K * limit / "
+                            "flops) >= 8 output channels (note column of parity.csv)",
                 "oracle_cpu_s": self.oracle_s, "unique_keys_checked": self.keys}
 
     @staticmethod
@@ -172,19 +214,23 @@ class OracleChecker:
 
 def main(argv=None) -> int:
     argv = sys.argv[1:] if argv is None else list(argv)
-    extra = {"--workers": 0, "--pending": 24}
+    extra = {"--workers": 0, "--pending": 24, "--max-oracle-gflop": 30}
     rest = []
     it = iter(argv)
     for a in it:
         if a in extra:
-            extra[a] = int(next(it))
+            extra[a] = float(next(it)) if a == "--max-oracle-gflop" else int(next(it))
         else:
             rest.append(a)
     sweep = _sweep_module()
 
     def factory(args, ranks):
-        workers = extra["--workers"] or max(1, (os.cpu_count() or 2) // ranks.world)
-        return OracleChecker(args.data_seed, workers, extra["--pending"])
+        # leave cores for the ranks' own host work (input generation, D2H, spooling)
+        workers = extra["--workers"] or max(1, (os.cpu_count() or 2) // ranks.world - 2)
+        os.makedirs(args.out, exist_ok=True)
+        return OracleChecker(args.data_seed, workers, extra["--pending"],
+                             journal=os.path.join(args.out, f"parity_rank{ranks.rank}.journal.csv"),
+                             max_oracle_flops=extra["--max-oracle-gflop"] * 1e9)
     return sweep.main(rest, checker_factory=factory, script=str(Path(__file__).resolve()),
                       relaunch_argv=argv)
 

@@ -437,3 +437,29 @@ def test_sweep_plan_classes_match_oracle(cuda):
                 e = _check_conv(d, fn(), ref)
                 worst[(name, path)] = max(worst.get((name, path), 0.0), e)
     print({f"{k[0]}/{k[1]}": f"{v:.1e}" for k, v in sorted(worst.items())})
+
+
+PROMOTE_KEYS = ["n1_c2048x28x28_f256x7x7_s1x1_p3x3_d1x1_g1_b0",     # C*R*S = 100352, few tiles
+                "n1_c2048x112x112_f128x3x3_s1x1_p1x1_d1x1_g1_b0",   # 18432, many whole tiles
+                "n1_c1024x28x28_f64x7x7_s2x2_p3x3_d1x1_g1_b0"]      # 50176, short grid (K parts)
+
+
+@pytest.mark.parametrize("key", PROMOTE_KEYS)
+def test_large_reductions_with_accumulator_promotion(cuda, key):
+    """The tcgen05 fp32 accumulation truncates: one accumulator over C*R*S = 100352 drifted
+    to 1.3e-3 (3xTF32) / 6e-4 (3xBF16) normalized error on the config-5 sweep.  Every
+    tensor-core path drains its accumulator every ~2-4K reduction elements (promote_k) and
+    adds the partials in fp32; all of them must now pass the gate on these reductions."""
+    from paper_2407_10730_b200.algos import (conv_baseline_im2col_gemm, conv_fused,
+                                             conv_main_blocked_direct)
+    from paper_2407_10730_b200.descriptor import parse_key
+    from paper_2407_10730_b200.timing import PhaseLedger
+    d = parse_key(key)
+    inp, (x, w, b) = _inputs(d)
+    ref = orc.conv_banded64(d, x, w, b).astype(np.float32)
+    errs = {}
+    for v in ("tc3xbf16", "tc3xtf32"):
+        errs[f"fused/{v}"] = _check_conv(d, conv_fused(inp, variant=v), ref)
+        errs[f"im2col/{v}"] = _check_conv(d, conv_baseline_im2col_gemm(inp, PhaseLedger(), variant=v), ref)
+        errs[f"sconv/{v}"] = _check_conv(d, conv_main_blocked_direct(inp, PhaseLedger(), variant=v), ref)
+    print(key, {k: f"{e:.1e}" for k, e in errs.items()})

@@ -77,3 +77,39 @@ def test_model_op_set_is_valid():
     for k in data["unique"]:
         assert key_of(parse_key(k)) == k
     assert data["models"]["resnet50"]["layers"][0].startswith("n1_c3x224x224_f64x7x7_s2x2_p3x3")
+
+
+def test_charts_from_report_csvs(tmp_path):
+    """tools/charts.py renders the reference report's speedup and breakdown CSVs as SVG:
+    one bar per op (blue >= 1, red < 1), stacked phases per side; byte-identical reruns."""
+    import xml.etree.ElementTree as ET
+    spec = importlib.util.spec_from_file_location("charts_tool", ROOT / "tools" / "charts.py")
+    charts = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(charts)
+    sp = tmp_path / "speedup.csv"
+    sp.write_text("key,flops,operation_speedup,convolution_speedup\n"
+                  "a,10,2.0,1.5\nb,30,0.5,0.8\nc,20,1.0,3.0\n")
+    bd = tmp_path / "breakdown.csv"
+    cols = ["index", "key", "side"] + [f"{s}_ms" for s in charts.PHASE_STEMS] + ["operation_ms"]
+    lines = [",".join(cols)]
+    for i in range(2):
+        for side in ("main", "baseline"):
+            lines.append(",".join([str(i), f"k{i}", side] + ["0.5"] * 7 + ["3.5"]))
+    bd.write_text("\n".join(lines) + "\n")
+    for args in (["speedup", "--in", str(sp), "--out", str(tmp_path / "s.svg"), "--sort", "by-flops"],
+                 ["speedup", "--in", str(sp), "--out", str(tmp_path / "l.svg"), "--log-y",
+                  "--scope", "operation"],
+                 ["breakdown", "--in", str(bd), "--out", str(tmp_path / "b.svg")]):
+        assert charts.main(args) == 0
+    s = (tmp_path / "s.svg").read_text()
+    root = ET.fromstring(s)
+    fills = [e.get("fill") for e in root.iter("{http://www.w3.org/2000/svg}rect")][1:]
+    assert fills == [charts.SPEEDUP_COLOR, charts.SPEEDUP_COLOR, charts.SLOWDOWN_COLOR]  # by flops
+    ET.fromstring((tmp_path / "l.svg").read_text())
+    b = ET.fromstring((tmp_path / "b.svg").read_text())
+    assert len(list(b.iter("{http://www.w3.org/2000/svg}rect"))) == 1 + 2 * 2 * 7 + 7
+    assert charts.main(["speedup", "--in", str(sp), "--out", str(tmp_path / "s2.svg"),
+                        "--sort", "by-flops"]) == 0
+    assert (tmp_path / "s2.svg").read_bytes() == (tmp_path / "s.svg").read_bytes()
+    (tmp_path / "bad.csv").write_text("key,flops\n")
+    assert charts.main(["speedup", "--in", str(tmp_path / "bad.csv"), "--out", str(tmp_path / "x.svg")]) == 1

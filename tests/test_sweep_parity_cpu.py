@@ -46,3 +46,26 @@ def test_oracle_checker_scores_outputs(tmp_path):
     rows = list(csv.DictReader(open(tmp_path / "p.csv")))
     assert [(r["index"], r["mode"]) for r in rows] == [("0", "fused"), ("0", "main"),
                                                        ("3", "baseline"), ("7", "fused")]
+
+
+def test_channel_subset_oracle_for_large_ops(tmp_path):
+    """Ops above the oracle budget are checked on a seeded subset of output channels (every
+    pixel of each): the subset oracle equals those channels of the full oracle."""
+    sp = _mod()
+    d = ConvDescriptor(batch=1, in_channels=16, in_h=10, in_w=10, out_channels=40, k_h=3, k_w=3,
+                       pad_h=1, pad_w=1)
+    from paper_2407_10730_b200.descriptor import flop_count
+    assert sp.oracle_channels(d, flop_count(d)) is None
+    ch = sp.oracle_channels(d, flop_count(d) / 10)
+    assert len(ch) == 8 and (np.diff(ch) > 0).all()
+    assert np.array_equal(ch, sp.oracle_channels(d, flop_count(d) / 10))  # seeded
+    x, w, b = orc.make_inputs(d, 0)
+    y = orc.conv_direct_naive(d, x, w, b)
+    y_bad = y.copy()
+    y_bad[0, ch[3], 4, 4] += 0.5
+    np.save(tmp_path / "a.npy", y)
+    np.save(tmp_path / "b.npy", y_bad)
+    res = sp._check_job(d, 0, [(0, "fused", str(tmp_path / "a.npy")),
+                               (1, "fused", str(tmp_path / "b.npy"))], ch)
+    assert res[0][2] < 1e-7 and "8/40 channels" in res[0][4]
+    assert abs(res[1][2] - 0.5 / np.sqrt(16 * 9)) < 1e-6

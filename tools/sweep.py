@@ -95,6 +95,7 @@ def parser() -> argparse.ArgumentParser:
     ap.add_argument("--graph", action="store_true",
                     help="time each op as a replayed CUDA graph (kernels without host launch gaps)")
     ap.add_argument("--max-gflop", type=float, default=0.0, help="skip larger ops (0: none)")
+    ap.add_argument("--min-gflop", type=float, default=0.0, help="skip smaller ops")
     ap.add_argument("--out", default="sweep_out")
     ap.add_argument("--verbose", action="store_true", help="print every op key before it runs")
     ap.add_argument("--limit", type=int, default=0, help="diagnostics: run at most N ops per rank")
@@ -114,6 +115,8 @@ def select_ops(args):
     idx = stratified_sample(descs, args.sample, args.seed) if args.sample else list(range(len(descs)))
     if args.max_gflop > 0:
         idx = [i for i in idx if flop_count(descs[i]) <= args.max_gflop * 1e9]
+    if args.min_gflop > 0:
+        idx = [i for i in idx if flop_count(descs[i]) > args.min_gflop * 1e9]
     return descs, idx, model_ops
 
 
@@ -183,8 +186,9 @@ def run(args, checker=None, ranks=None) -> int:
             checker.check(d, host, outs)
         del outs, dev
         n += len(group)
-        if rank == 0 and (n // 100) != ((n - len(group)) // 100):
-            print(f"[rank0] {n}/{len(mine)} ops, {time.time() - t0:.0f} s", flush=True)
+        if rank == 0 and (n // 50) != ((n - len(group)) // 50):
+            extra = checker.progress() if checker is not None else ""
+            print(f"[rank0] {n}/{len(mine)} ops, {time.time() - t0:.0f} s {extra}", flush=True)
     torch.cuda.empty_cache()
     parity = checker.finish() if checker is not None else None
 
