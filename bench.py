@@ -431,6 +431,11 @@ def config_table(peaks, runs: int = 5):
                     lambda i, l: algos.conv_baseline_im2col_gemm(i, l)),
                    ("sconv", algos.DEFAULT_VARIANT,
                     lambda i, l: algos.conv_main_blocked_direct(i, l))]
+        if algos.DEFAULT_VARIANT != "tc3xtf32":  # the spec's 3xTF32 split, next to the default
+            algos_ += [("im2col_gemm_tf32", "tc3xtf32",
+                        lambda i, l: algos.conv_baseline_im2col_gemm(i, l, variant="tc3xtf32")),
+                       ("sconv_tf32", "tc3xtf32",
+                        lambda i, l: algos.conv_main_blocked_direct(i, l, variant="tc3xtf32"))]
         row = {}
         for tag, variant, fn in algos_:
             fn(inp, EventLedger())  # eager first call: plans, kernel attributes, tensor maps
@@ -464,13 +469,14 @@ def config_table(peaks, runs: int = 5):
                 ent["kernel_roofline_frac"] = rl["t_roofline_s"] / (k * 1e-9) if k else None
                 ent["target_60pct_met"] = bool(k and rl["t_roofline_s"] / (k * 1e-9) >= 0.6)
             else:
-                pk = st.phase_ns_mean[Phase.PRE_REORDER if tag == "im2col_gemm" else Phase.IN_PACKING]
-                ent["pack_kernel"] = "K1 im2col" if tag == "im2col_gemm" else "K2 slice pack"
+                im2 = tag.startswith("im2col_gemm")
+                pk = st.phase_ns_mean[Phase.PRE_REORDER if im2 else Phase.IN_PACKING]
+                ent["pack_kernel"] = "K1 im2col" if im2 else "K2 slice pack"
                 ent["pack_gbs"] = rl["pack_bytes"] / (pk * 1e-9) / 1e9 if pk else None
                 ent["pack_hbm_frac"] = rl["pack_bytes"] / (pk * 1e-9) / hbm if pk else None
                 ent["target_70pct_met"] = bool(pk and rl["pack_bytes"] / (pk * 1e-9) / hbm >= 0.7)
                 pack = st.phase_ns_mean[Phase.IN_PACKING] + (
-                    st.phase_ns_mean[Phase.PRE_REORDER] if tag == "im2col_gemm" else 0.0)
+                    st.phase_ns_mean[Phase.PRE_REORDER] if im2 else 0.0)
                 ent["pack_share"] = pack / op if op else None
             row[tag] = ent
         table[name] = row

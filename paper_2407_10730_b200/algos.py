@@ -44,10 +44,11 @@ from ._capi import UnsupportedDescriptorError
 from .descriptor import ConvDescriptor, flop_count, output_shape
 from .timing import HOST_PHASES, Phase, PhaseLedger
 
-# Stepwise algorithms default to the spec's 3xTF32; the fused hot path defaults to 3xBF16,
-# which on B200 runs at twice the MMA rate with half the operand bytes and measured a
-# lower, K-independent error.
-DEFAULT_VARIANT = "tc3xtf32"
+# Every tensor-core path defaults to 3xBF16: on B200 it runs at twice the 3xTF32 MMA rate
+# with half the operand bytes, and measured a lower, K-independent error (DESIGN.md
+# "Numerics").  The spec's 3xTF32 stays available everywhere (variant="tc3xtf32") and is
+# measured next to it in bench.py's per-config table.
+DEFAULT_VARIANT = "tc3xbf16"
 FUSED_DEFAULT_VARIANT = "tc3xbf16"
 # "auto" (the fused entry points' default): the FFMA kernel for small convolutions -- one
 # launch on raw NCHW / OIHW, no split passes -- else 3xBF16.  On the config-5 sample, FFMA

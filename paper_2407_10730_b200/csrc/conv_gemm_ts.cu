@@ -23,14 +23,17 @@
 
 namespace cb {
 
+unsigned long long* debug_trace_buffer(int ctas, cudaStream_t st);  // conv_tma.cu
+
 constexpr int G8_BM = 128;
 constexpr int G8_PROD_WARPS = 8;
-constexpr int G8_EPI_WARP0 = 8;
-constexpr int G8_TMA_WARP = 12;
-constexpr int G8_MMA_WARP = 13;
-constexpr int G8_ATMA_WARP = 14;  // A tiles by TMA (matrix sources)
-constexpr int G8_THREADS = 15 * 32;
-constexpr int G8_ASTAGES = 4;
+constexpr int G8_EPI_WARP0 = 8;   // warps 8-15: two epilogue warps per TMEM lane quadrant
+constexpr int G8_EPI_THREADS = 256;
+constexpr int G8_TMA_WARP = 16;
+constexpr int G8_MMA_WARP = 17;
+constexpr int G8_ATMA_WARP = 18;  // A tiles by TMA (matrix sources)
+constexpr int G8_THREADS = 19 * 32;
+constexpr int G8_ASTAGES_MAX = 8;
 constexpr int G8_ASTAGE_BYTES = 32 * G8_BM * 4;  // [32 k][128 px] fp32
 constexpr int G8_TMEM_COLS = 512;
 constexpr int G8_CK = 32;  // reduction elements per A chunk
@@ -62,7 +65,31 @@ struct G8Params {
     // chunks (of 32 reduction elements) the accumulator is drained by the epilogue and
     // added to the output in fp32 (round to nearest), then restarted.
     int range_chunks;
+    unsigned long long* trace;  // diagnostics (CB_K8_TRACE): per-CTA globaltimer stamps
+    int astages;                // A chunk stages in smem (TMA sources)
+    int debug;                  // diagnostics (CB_K8_DEBUG): 1 no weight TMA, 2 no A TMA, 4 no MMA, 8 no A build
 };
+
+// CB_K8_TRACE chunk stamps of CTA 0 (chunk cg < 256): [8192 + 4 cg + e], e: 0 A TMA
+// issued, 1 producer group saw the A stage, 2 producer arrived a_full, 3 MMA saw a_full
+__device__ __forceinline__ void g8_cstamp(const struct G8Params& p, int64_t cg, int e);
+// CB_K8_TRACE stamps, [cta][32]: slot li*6 + e for the CTA's local item li < 5 (e: 0/1
+// producer warp 0 starts / finishes the item, 2/3 MMA first chunk issued / last commit,
+// 4/5 epilogue accumulator ready / last store issued), 30 kernel end, 31 kernel start
+__device__ __forceinline__ void g8_stamp(const G8Params& p, int slot) {
+    if (p.trace && slot < 32) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[blockIdx.x * 32 + slot] = t;
+    }
+}
+__device__ __forceinline__ void g8_cstamp(const G8Params& p, int64_t cg, int e) {
+    if (p.trace && blockIdx.x == 0 && cg < 256) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8192 + 4 * cg + e] = t;
+    }
+}
 
 // channel range [lo, hi) of part `sub` of a BN-wide tile cut into `parts` (16-aligned)
 __device__ __forceinline__ int g8_part_col(int bn, int parts, int sub) {
@@ -91,16 +118,16 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     float* astage = reinterpret_cast<float*>(smem + p.bstages * Cfg::STAGE_BYTES);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bstages * Cfg::STAGE_BYTES +
-                                                 G8_ASTAGES * G8_ASTAGE_BYTES);
+                                                 p.astages * G8_ASTAGE_BYTES);
     uint64_t* b_full = bars;                    // [bstages]
     uint64_t* b_empty = b_full + p.bstages;     // [bstages]
     uint64_t* a_full = b_empty + p.bstages;     // [ring]
     uint64_t* a_empty = a_full + p.ring;        // [ring]
     uint64_t* acc_full = a_empty + p.ring;      // 1
     uint64_t* acc_empty = acc_full + 1;         // 1
-    uint64_t* as_full = acc_empty + 1;          // [G8_ASTAGES]
-    uint64_t* as_empty = as_full + G8_ASTAGES;  // [G8_ASTAGES]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(as_empty + G8_ASTAGES);
+    uint64_t* as_full = acc_empty + 1;          // [astages]
+    uint64_t* as_empty = as_full + p.astages;   // [astages]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(as_empty + p.astages);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -116,8 +143,8 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             ptx::mbar_init(&a_empty[s], 1);
         }
         ptx::mbar_init(acc_full, 1);
-        ptx::mbar_init(acc_empty, 128);
-        for (int s = 0; s < G8_ASTAGES; ++s) {
+        ptx::mbar_init(acc_empty, G8_EPI_THREADS);
+        for (int s = 0; s < p.astages; ++s) {
             ptx::mbar_init(&as_full[s], 1);
             ptx::mbar_init(&as_empty[s], 128);
         }
@@ -133,6 +160,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int nch = p.nchunks;
+    if (threadIdx.x == 0) g8_stamp(p, 31);
 
     // pixel tile mt, row m -> launch-local pixel jl (slice-aligned tiles for slice sources)
     auto pix_of = [&](int64_t mt, int m, int64_t& jl) -> bool {
@@ -169,10 +197,30 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         const int m = quad * 32 + lane;
         const uint32_t lane_tm = tmem_base + ((uint32_t)(quad * 32) << 16) + BN;  // ring base
         int64_t cbase = 0;  // chunks this CTA produced before the current item
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch) {
+        int li = 0;
+        // This group's next global chunk cg (cg == kpar mod 2) and its TMEM ring slot / A
+        // stage with their phases, advanced incrementally: per-chunk 64-bit div/mod by the
+        // runtime ring and stage counts had cost ~1300 cycles a chunk on the MMA's critical
+        // path (K8's MMAs ran at ~45% of the tcgen05 rate with every operand disabled).
+        int64_t cg = kpar;
+        int slot = kpar % p.ring, as = kpar;  // astages is even (>= 2)
+        uint32_t ph = (uint32_t)(kpar / p.ring), asph = 0;
+        auto advance = [&] {
+            cg += 2;
+            if ((slot += 2) >= p.ring) {
+                slot -= p.ring;
+                ph ^= 1;
+            }
+            if ((as += 2) >= p.astages) {
+                as -= p.astages;
+                asph ^= 1;
+            }
+        };
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch, ++li) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
+            if (threadIdx.x == 0 && li < 5) g8_stamp(p, li * 6);
             int64_t jl;
             const bool jvalid = pix_of(mt, m, jl);
             int64_t lbase = 0, lstride = 0;
@@ -183,16 +231,21 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             // (cg % 4) is then always consumed by the same group, so its phase parity can never
             // alias an older phase (with kc parity, an odd chunk count per item would hand a
             // stage to the other group on the next item -- an ABA race on the mbarrier phase)
-            for (int kc = (int)((kpar - cbase) & 1); kc < nch; kc += 2) {
-                const int64_t cg = cbase + kc;
-                const int slot = (int)(cg % p.ring);
-                const uint32_t ph = (uint32_t)((cg / p.ring) & 1);
+            for (int kc = (int)(cg - cbase); kc < nch; kc += 2) {
                 float v[G8_CK];
                 const int k0 = kc * G8_CK;
                 if (p.tma_a) {  // the chunk's [32 k][128 px] box is in smem: read column m
-                    const int as = (int)(cg % G8_ASTAGES);
-                    ptx::mbar_wait(&as_full[as], (uint32_t)((cg / G8_ASTAGES) & 1));
+                    ptx::mbar_wait(&as_full[as], asph);
+                    if (lane == 0 && quad == 0) g8_cstamp(p, cg, 1);
                     const float* col = astage + (size_t)as * (32 * G8_BM) + m;
+                    if (p.debug & 8) {  // diagnostics: no A build (stale TMEM A)
+                        ptx::mbar_arrive(&as_empty[as]);
+                        ptx::mbar_wait(&a_empty[slot], ph ^ 1);
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(&a_full[slot]);
+                        advance();
+                        continue;
+                    }
 #pragma unroll
                     for (int e = 0; e < G8_CK; ++e) v[e] = col[e * G8_BM];
                     ptx::mbar_arrive(&as_empty[as]);
@@ -234,14 +287,21 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&a_full[slot]);
+                if (lane == 0 && quad == 0) g8_cstamp(p, cg, 2);
+                advance();
             }
+            if (threadIdx.x == 0 && li < 5) g8_stamp(p, li * 6 + 1);
         }
     } else if (warp < G8_TMA_WARP) {
         // ============================ epilogue ==========================================
-        const int quad = warp & 3;
+        // Two warps per lane quadrant, alternating 32-column chunks: the single accumulator
+        // is released only once it is fully read, and each warp's reads wait behind its own
+        // stores, so a second warp halves the time the MMAs of the next item wait for it.
+        const int quad = warp & 3, ehalf = (warp - G8_EPI_WARP0) >> 2;
         const int m = quad * 32 + lane;
         int i = 0;  // accumulator ranges drained so far (acc_full phase)
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x) {
+        int li = 0;
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++li) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
@@ -256,17 +316,18 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             for (int rg = 0; rg < nranges; ++rg, ++i) {
             ptx::mbar_wait(acc_full, i & 1);
             ptx::tc_fence_after();
-            if (ncol <= 0) {  // no valid channel in this item: release the accumulator anyway
+            if (threadIdx.x == G8_EPI_WARP0 * 32 && rg == 0 && li < 5) g8_stamp(p, li * 6 + 4);
+            if (32 * ehalf >= ncol) {  // no column chunk for this warp: release at once
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(acc_empty);
             }
             const bool add = p.add_mode || rg > 0;  // later ranges add to the first's store
 #pragma unroll 1
-            for (int c0 = 0; c0 < ncol; c0 += 32) {
+            for (int c0 = 32 * ehalf; c0 < ncol; c0 += 64) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, r);
                 ptx::tmem_ld_wait();
-                if (c0 + 32 >= ncol) {  // accumulator fully read: the next range may start
+                if (c0 + 64 >= ncol) {  // this warp's part of the accumulator is read
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(acc_empty);
                 }
@@ -290,12 +351,15 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 }
             }
             }
+            if (threadIdx.x == G8_EPI_WARP0 * 32 && li < 5) g8_stamp(p, li * 6 + 5);
         }
     } else if (warp == G8_ATMA_WARP) {
         // ============================ A chunks by TMA (matrix sources) ==================
         if (p.tma_a) {
             const uint32_t leader = ptx::elect_one();
             int64_t cbase = 0;
+            int as = 0;
+            uint32_t asph = 0;
             for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch) {
                 int nt, gi;
                 int64_t mt;
@@ -304,11 +368,14 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 const int row0 = gi * g.kdim;
                 const int64_t sl = p.tps ? mt / p.tps : 0;
                 const int xs = p.tps ? (int)(mt - sl * p.tps) * G8_BM : 0;
-                for (int kc = 0; kc < nch; ++kc) {
+                for (int kc = 0; kc < nch; ++kc, as = as + 1 == p.astages ? 0 : as + 1,
+                         asph ^= (as == 0 ? 1u : 0u)) {
                     const int64_t cg = cbase + kc;
-                    const int as = (int)(cg % G8_ASTAGES);
-                    ptx::mbar_wait(&as_empty[as], (uint32_t)(((cg / G8_ASTAGES) & 1) ^ 1));
-                    if (leader) {
+                    ptx::mbar_wait(&as_empty[as], asph ^ 1);
+                    if (leader) g8_cstamp(p, cg, 0);
+                    if (leader && (p.debug & 2) && cg >= p.astages) {
+                        ptx::mbar_arrive(&as_full[as]);  // diagnostics: stale A chunk
+                    } else if (leader) {
                         ptx::mbar_arrive_expect_tx(&as_full[as], G8_ASTAGE_BYTES);
                         if (p.tps)  // slice buffer as {np, kdim, slices}
                             ptx::tma_load_3d(astage + (size_t)as * (32 * G8_BM), &tm_a, &as_full[as], xs,
@@ -326,17 +393,19 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         const uint32_t leader = ptx::elect_one();
         const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
         int64_t sbase = 0;
+        int s = 0;
+        uint32_t ph = 0;
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, sbase += nstage) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
             const int row0 = gi * g.kpg + nt * BN + c_lo;  // (a part's rows start the stage)
-            for (int kb = 0; kb < nstage; ++kb) {
+            for (int kb = 0; kb < nstage; ++kb, s = s + 1 == p.bstages ? 0 : s + 1, ph ^= (s == 0 ? 1u : 0u)) {
                 const int64_t sg = sbase + kb;
-                const int s = (int)(sg % p.bstages);
-                const uint32_t ph = (uint32_t)((sg / p.bstages) & 1);
                 ptx::mbar_wait(&b_empty[s], ph ^ 1);
-                if (leader) {
+                if (leader && (p.debug & 1) && sg >= p.bstages) {
+                    ptx::mbar_arrive(&b_full[s]);  // diagnostics: stale weights, no transfer
+                } else if (leader) {
                     uint8_t* st = smem + s * Cfg::STAGE_BYTES;
                     ptx::mbar_arrive_expect_tx(&b_full[s], Cfg::STAGE_BYTES);
                     ptx::tma_load_2d(st, &tm_hi, &b_full[s], kb * Cfg::KE, row0);
@@ -353,15 +422,18 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
         const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
         int64_t cbase = 0, sbase = 0;
+        int slot = 0, s = 0;  // TMEM A ring slot and weight stage, with their phases
+        uint32_t aph = 0, bph = 0;
         int i = 0;  // accumulator ranges issued so far (acc_empty phase)
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch, sbase += nstage) {
+        int li = 0;
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch, sbase += nstage, ++li) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
             const uint32_t idesc =
                 c_hi - c_lo == BN ? idesc_full : ptx::idesc_f32acc<BF16>(G8_BM, c_hi - c_lo);
+            int kr = 0;  // position inside the accumulator range
             for (int kc = 0; kc < nch; ++kc) {
-                const int kr = kc % p.range_chunks;  // position inside the accumulator range
                 if (kr == 0) {  // a fresh accumulator range: the epilogue drained the last one
                     if (kc > 0) {
                         if (leader) ptx::umma_commit(acc_full);
@@ -372,18 +444,17 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                     ptx::tc_fence_after();
                 }
                 const int64_t cg = cbase + kc;
-                const int slot = (int)(cg % p.ring);
-                const int64_t sg = sbase + kc / Cfg::CPS;
-                const int s = (int)(sg % p.bstages);
-                if (kc % Cfg::CPS == 0) ptx::mbar_wait(&b_full[s], (uint32_t)((sg / p.bstages) & 1));
-                ptx::mbar_wait(&a_full[slot], (uint32_t)((cg / p.ring) & 1));
+                if (kc % Cfg::CPS == 0) ptx::mbar_wait(&b_full[s], bph);
+                ptx::mbar_wait(&a_full[slot], aph);
                 ptx::tc_fence_after();
+                if (leader && kc == 0 && li < 5) g8_stamp(p, li * 6 + 2);
+                if (leader) g8_cstamp(p, cg, 3);
                 if (leader) {
                     const uint32_t a_hi = tmem_base + BN + slot * Cfg::CHUNK_COLS;
                     const uint32_t a_lo = a_hi + Cfg::HALF_COLS;
                     const uint64_t sb = db0 + (uint64_t)(s * STG16) + (kc % Cfg::CPS) * (G8_CK * Cfg::EB / 16);
 #pragma unroll
-                    for (int u = 0; u < G8_CK / Cfg::UK; ++u) {
+                    for (int u = 0; u < G8_CK / Cfg::UK && !(p.debug & 4); ++u) {
                         const uint64_t dbh = sb + 2 * u, dbl = dbh + BLO16;
                         const uint32_t first = (kr > 0 || u > 0) ? 1u : 0u;
                         ptx::umma_ts<BF16>(tmem_base, a_lo + u * 8, dbh, idesc, first);
@@ -394,8 +465,18 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                     if (kc % Cfg::CPS == Cfg::CPS - 1 || kc == nch - 1) ptx::umma_commit(&b_empty[s]);
                 }
                 __syncwarp();
+                if (++slot == p.ring) {
+                    slot = 0;
+                    aph ^= 1;
+                }
+                if ((kc % Cfg::CPS == Cfg::CPS - 1 || kc == nch - 1) && ++s == p.bstages) {
+                    s = 0;
+                    bph ^= 1;
+                }
+                if (++kr == p.range_chunks) kr = 0;
             }
             if (leader) ptx::umma_commit(acc_full);
+            if (leader && li < 5) g8_stamp(p, li * 6 + 3);
             __syncwarp();
             ++i;
         }
@@ -403,6 +484,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
 
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) g8_stamp(p, 30);
     if (warp == G8_MMA_WARP) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, G8_TMEM_COLS);
@@ -430,10 +512,15 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
     using Cfg = G8Cfg<BN, BF16>;
     G8Params prm = prm_in;
     prm.ring = (G8_TMEM_COLS - BN) / Cfg::CHUNK_COLS;
-    prm.bstages = std::min(8, (200 * 1024 - G8_ASTAGES * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
+    prm.astages = 4;
+    if (const char* e = std::getenv("CB_K8_ASTAGES"))  // even: each stage stays with one producer group
+        prm.astages = std::max(2, std::min(G8_ASTAGES_MAX, std::atoi(e))) & ~1;
+    prm.bstages = std::min(8, (225 * 1024 - prm.astages * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
+    if (const char* e = std::getenv("CB_K8_DEBUG")) prm.debug = std::atoi(e);
     if (const char* e = std::getenv("CB_K8_BSTAGES")) prm.bstages = std::max(2, std::min(prm.bstages, std::atoi(e)));
-    const size_t smem = 1024 + (size_t)prm.bstages * Cfg::STAGE_BYTES + G8_ASTAGES * G8_ASTAGE_BYTES +
-                        8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * G8_ASTAGES);
+    if (prm.bstages < 2) return fail(CB_ERR_UNSUPPORTED, "K8: shared memory for 2 weight stages");
+    const size_t smem = 1024 + (size_t)prm.bstages * Cfg::STAGE_BYTES + prm.astages * G8_ASTAGE_BYTES +
+                        8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * prm.astages);
     auto kern = gemm_ts_kernel<BN, BF16>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -483,6 +570,7 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
             return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)r));
     }
     const int grid = (int)std::min<int64_t>(prm.items, sm_count());
+    if (std::getenv("CB_K8_TRACE")) prm.trace = debug_trace_buffer(1024, st);  // + chunk stamps
     kern<<<grid, G8_THREADS, std::max<size_t>(smem, 120 * 1024), st>>>(prm, mh, ml, ma);
     return check_launch("gemm_ts_kernel");
 }

@@ -22,6 +22,39 @@ from paper_2407_10730_b200 import _capi, algos
 from paper_2407_10730_b200.configs import CONFIGS, conv_flops
 
 
+_FLUSH = []
+
+
+def cold_time(fn, reps: int) -> float:
+    """us per launch of fn with the L2 flushed before each launch (a 256 MB write, then a
+    256 MB read so the flush lines are clean): one graph of reps x (flush, fn) minus one
+    graph of reps x flush."""
+    if not _FLUSH:
+        _FLUSH.extend([torch.empty(64 << 20, device="cuda"), torch.ones(64 << 20, device="cuda")])
+    fw, fr = _FLUSH
+
+    def flush():
+        fw.zero_()
+        fr.sum()
+    out = []
+    for with_fn in (True, False):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                flush()
+                if with_fn:
+                    fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) / reps * 1e3)
+    return out[0] - out[1]
+
+
 def run(name: str, variant: str, reps: int = 20) -> None:
     d = CONFIGS[name]
     if os.environ.get("CB_KT_BATCH"):  # diagnostics: same layer, another batch size
@@ -80,6 +113,8 @@ def run(name: str, variant: str, reps: int = 20) -> None:
             sampler.__exit__(None, None, None)
             clk = sampler.summary()
         res[label] = e0.elapsed_time(e1) / reps * 1e3
+        if os.environ.get("CB_KT_COLD"):  # L2-cold: T(flush + launch) - T(flush), per launch
+            res[label + "cold"] = cold_time(fn, reps)
     if clk:
         print(f"   clocks during K6: {clk}")
     t6 = res["K6"] * 1e-6

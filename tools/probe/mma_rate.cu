@@ -11,6 +11,7 @@
 using namespace cb;
 
 constexpr int ITER = 4096;
+__device__ int g_rand = 0;
 
 template <int TS, int N, int SIDE>  // SIDE: 0 none, 1 tcgen05.ld loop, 2 tcgen05.st loop
 __global__ void __launch_bounds__(192, 1) mma_rate(unsigned long long* out) {
@@ -21,7 +22,8 @@ __global__ void __launch_bounds__(192, 1) mma_rate(unsigned long long* out) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 16384 + 256 * 128);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
     volatile uint32_t* done = slot + 1;
-    for (int i = threadIdx.x; i < (16384 + N * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    for (int i = threadIdx.x; i < (16384 + N * 128) / 4; i += blockDim.x)  // random bf16 in [0.5, 1) or zeros
+        reinterpret_cast<uint32_t*>(smem)[i] = g_rand ? (((uint32_t)i * 2654435761u) & 0x007f007fu) | 0x3f003f00u : 0u;
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         ptx::mbar_init(bar, 1); ptx::mbar_init(bar + 2, 1); ptx::mbar_init(bar + 3, 1);
@@ -125,5 +127,10 @@ int main() {
     run<0, 64, 1>(d); run<0, 64, 2>(d);
     run<1, 64, 3>(d); run<1, 64, 4>(d); run<1, 128, 3>(d); run<0, 64, 3>(d);
     run<1, 256, 5>(d); run<1, 64, 5>(d); run<1, 256, 6>(d); run<1, 64, 6>(d);
+    run<1, 256, 1>(d); run<1, 256, 2>(d);
+    int one = 1;
+    cudaMemcpyToSymbol(g_rand, &one, sizeof(int));
+    printf("random operands:\n");
+    run<0, 256, 0>(d); run<1, 256, 0>(d); run<1, 256, 2>(d); run<1, 128, 0>(d); run<1, 64, 0>(d);
     return 0;
 }
