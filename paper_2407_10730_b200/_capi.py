@@ -9,12 +9,15 @@ point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .descriptor import ConvDescriptor, InvalidDescriptorError
 
-LIB_PATH = Path(__file__).resolve().parent / "libconvb200.so"
+# CB_LIB_PATH (diagnostics only): load another build of the library for A/B runs
+LIB_PATH = Path(os.environ["CB_LIB_PATH"]) if os.environ.get("CB_LIB_PATH") else \
+    Path(__file__).resolve().parent / "libconvb200.so"
 
 CB_OK, CB_ERR_INVALID, CB_ERR_UNSUPPORTED, CB_ERR_WORKSPACE, CB_ERR_MISALIGNED, CB_ERR_CUDA = range(6)
 

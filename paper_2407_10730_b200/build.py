@@ -35,15 +35,18 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA source into one shared library next to this file."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
+    """Compile every CUDA source into one shared library next to this file.  `defines` /
+    `out` build a diagnostics variant elsewhere (e.g. -DCB_MBAR_HINT into _ab/, loaded with
+    CB_LIB_PATH for A/B runs)."""
+    lib_out = Path(out) if out else LIB
+    if not force and not defines and not _stale():
         return LIB
-    objdir = PKG / "_build"
+    objdir = PKG / ("_build" if not defines else "_build_" + "_".join(d.strip("-D") for d in defines))
     objdir.mkdir(exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", str(ROOT / "include"), "-I", str(CSRC), "--expt-relaxed-constexpr",
-              "-Xptxas", "-v" if verbose else "-O3"]
+              "-Xptxas", "-v" if verbose else "-O3", *defines]
     shared = [CSRC / h for h in HEADERS] + [ROOT / "include" / "convb200.h", Path(__file__)]
     newest_shared = max(p.stat().st_mtime for p in shared)
 
@@ -63,7 +66,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB.with_suffix(".so.tmp")
+    lib_out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = lib_out.with_suffix(".so.tmp")
     # only the C ABI (cb_*) is exported: the static cudart and the C++ internals stay private
     vscript = objdir / "exports.map"
     vscript.write_text("{ global: cb_*; local: *; };\n")
@@ -72,8 +76,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
+
+
+def trace_lib() -> Path:
+    """The diagnostics build with the per-CTA timelines compiled in (-DCB_TRACE), for the
+    trace tools (CB_LIB_PATH)."""
+    out = ROOT / "_ab" / "libconvb200_trace.so"
+    srcs = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "convb200.h", Path(__file__)]
+    if out.exists() and out.stat().st_mtime > max(p.stat().st_mtime for p in srcs):
+        return out
+    return build(defines=("-DCB_TRACE",), out=out)
 
 
 if __name__ == "__main__":

@@ -9,6 +9,15 @@
 
 namespace cb {
 
+// Diagnostics timelines (CB_TMA_TRACE / CB_TS_TRACE / CB_K8_TRACE) exist only in a build with
+// -DCB_TRACE (build(defines=("-DCB_TRACE",)), loaded with CB_LIB_PATH): in the product build
+// every stamp and the conditions around it compile away.
+#ifdef CB_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
+
 // ------------------------------------------------------------------------------------
 // Error reporting (thread-local; returned through cb_last_error_string()).
 // ------------------------------------------------------------------------------------

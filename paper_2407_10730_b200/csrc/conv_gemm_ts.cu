@@ -59,6 +59,14 @@ struct G8Params {
     // item each, so the last wave keeps every SM busy.  A is rebuilt per range.
     int64_t full_items;
     int tail_split;
+    // Tail K-split (tail_k = 1, instead of the N split): each tail tile is cut into
+    // tail_split balanced ranges of its reduction chunks, one item each (full N, A built once
+    // per chunk overall).  The parts run concurrently in the last wave (one per CTA) and add
+    // into y in part order: the warp of lane quadrant q for column chunk c of part p > 0
+    // waits until flags[(tau * col_chunks + c) * 4 + q] == p, adds, and hands on p + 1 (the
+    // last part resets it to 0) -- deterministic, no workspace.
+    int tail_k;
+    uint32_t* flags;
     // Accumulator promotion: the tensor core's fp32 accumulation truncates, so its error
     // grows faster than linearly with the number of MMAs into one accumulator (measured on
     // the config-5 sweep: up to 1.3e-3 normalized at C*R*S = 100352).  Every range_chunks
@@ -67,8 +75,23 @@ struct G8Params {
     int range_chunks;
     unsigned long long* trace;  // diagnostics (CB_K8_TRACE): per-CTA globaltimer stamps
     int astages;                // A chunk stages in smem (TMA sources)
-    int debug;                  // diagnostics (CB_K8_DEBUG): 1 no weight TMA, 2 no A TMA, 4 no MMA, 8 no A build
+    int debug;                  // diagnostics (CB_K8_DEBUG): 1 no weight TMA, 2 no A TMA, 4 no MMA, 8 no A build, 16 no epilogue stores, 32 no bias
 };
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* f) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* f, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+
+// Hand-off flags of the K-split tail (G8Params::tail_k), a static pool: every launch takes
+// the next free run of slots (host side, round robin) and leaves them at 0.  Two K8 launches
+// running at the same time only share slots after 64K slots of other launches.
+constexpr int G8_FLAG_SLOTS = 1 << 16;
+__device__ uint32_t g8_flags[G8_FLAG_SLOTS];
 
 // CB_K8_TRACE chunk stamps of CTA 0 (chunk cg < 256): [8192 + 4 cg + e], e: 0 A TMA
 // issued, 1 producer group saw the A stage, 2 producer arrived a_full, 3 MMA saw a_full
@@ -77,14 +100,14 @@ __device__ __forceinline__ void g8_cstamp(const struct G8Params& p, int64_t cg, 
 // producer warp 0 starts / finishes the item, 2/3 MMA first chunk issued / last commit,
 // 4/5 epilogue accumulator ready / last store issued), 30 kernel end, 31 kernel start
 __device__ __forceinline__ void g8_stamp(const G8Params& p, int slot) {
-    if (p.trace && slot < 32) {
+    if (kTrace && p.trace && slot < 32) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[blockIdx.x * 32 + slot] = t;
     }
 }
 __device__ __forceinline__ void g8_cstamp(const G8Params& p, int64_t cg, int e) {
-    if (p.trace && blockIdx.x == 0 && cg < 256) {
+    if (kTrace && p.trace && blockIdx.x == 0 && cg < 256) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8192 + 4 * cg + e] = t;
@@ -174,16 +197,27 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         return jl < p.pm.j_count;
     };
     // item -> (channel tile nt, pixel tile mt, group gi; tile columns [c_lo, c_hi))
-    int c_lo = 0, c_hi = BN;
+    // K-split tail parts: reduction chunks [k_lo, k_hi), part index and tail tile tau
+    int c_lo = 0, c_hi = BN, k_lo = 0, k_hi = nch, kpart = -1, ktau = 0;
     auto decode = [&](int64_t t, int& nt, int64_t& mt, int& gi) {
         c_lo = 0;
         c_hi = BN;
+        k_lo = 0;
+        k_hi = nch;
+        kpart = -1;
         if (t >= p.full_items) {
             const int64_t j = t - p.full_items;
             const int sub = (int)(j % p.tail_split);
             t = p.full_items + j / p.tail_split;
-            c_lo = g8_part_col(BN, p.tail_split, sub);
-            c_hi = g8_part_col(BN, p.tail_split, sub + 1);
+            if (p.tail_k) {
+                kpart = sub;
+                ktau = (int)(j / p.tail_split);
+                k_lo = nch * sub / p.tail_split;
+                k_hi = nch * (sub + 1) / p.tail_split;
+            } else {
+                c_lo = g8_part_col(BN, p.tail_split, sub);
+                c_hi = g8_part_col(BN, p.tail_split, sub + 1);
+            }
         }
         nt = (int)(t % p.n_tiles);
         const int64_t r = t / p.n_tiles;
@@ -216,7 +250,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 asph ^= 1;
             }
         };
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch, ++li) {
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += k_hi - k_lo, ++li) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
@@ -231,7 +265,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             // (cg % 4) is then always consumed by the same group, so its phase parity can never
             // alias an older phase (with kc parity, an odd chunk count per item would hand a
             // stage to the other group on the next item -- an ABA race on the mbarrier phase)
-            for (int kc = (int)(cg - cbase); kc < nch; kc += 2) {
+            for (int kc = k_lo + (int)(cg - cbase); kc < k_hi; kc += 2) {
                 float v[G8_CK];
                 const int k0 = kc * G8_CK;
                 if (p.tma_a) {  // the chunk's [32 k][128 px] box is in smem: read column m
@@ -311,7 +345,8 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             if (jvalid) dst_linear(g, p.pm, p.pm.j_begin + jl, obase, ostride);
             const int f_tile0 = nt * BN + c_lo;
             const int ncol = min(c_hi - c_lo, g.kpg - f_tile0);
-            const int nranges = (nch + p.range_chunks - 1) / p.range_chunks;
+            const int nranges = (k_hi - k_lo + p.range_chunks - 1) / p.range_chunks;
+            const bool kord = kpart >= 0;  // K-split tail part (one range): ordered adds
 #pragma unroll 1
             for (int rg = 0; rg < nranges; ++rg, ++i) {
             ptx::mbar_wait(acc_full, i & 1);
@@ -321,7 +356,8 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(acc_empty);
             }
-            const bool add = p.add_mode || rg > 0;  // later ranges add to the first's store
+            // later ranges, and later K parts, add to what is already stored
+            const bool add = p.add_mode || rg > 0 || kpart > 0;
 #pragma unroll 1
             for (int c0 = 32 * ehalf; c0 < ncol; c0 += 64) {
                 uint32_t r[32];
@@ -331,7 +367,13 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(acc_empty);
                 }
-                if (!jvalid) continue;
+                uint32_t* flag = kord ? p.flags + ((size_t)(ktau * (BN / 32) + c0 / 32) * 4 + quad) : nullptr;
+                if (kord && kpart > 0) {  // the previous part's rows of this chunk are stored
+                    if (lane == 0)
+                        while (ld_acquire_gpu(flag) != (uint32_t)kpart) __nanosleep(64);
+                    __syncwarp();
+                }
+                if (jvalid && !(p.debug & 16)) {
                 const int nvalid = min(32, ncol - c0);
                 const int fb = gi * g.kpg + f_tile0 + c0;
                 float* dst = p.out + obase + (int64_t)fb * ostride;
@@ -347,7 +389,13 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                     for (int e = 0; e < 32; ++e)
                         if (e < nvalid)
                             dst[(int64_t)e * ostride] =
-                                __uint_as_float(r[e]) + (p.bias ? __ldg(p.bias + fb + e) : 0.f);
+                                __uint_as_float(r[e]) + (p.bias && !(p.debug & 32) ? __ldg(p.bias + fb + e) : 0.f);
+                }
+                }
+                if (kord) {  // hand the chunk on to the next part (the last one resets the flag)
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release_gpu(flag, kpart + 1 == p.tail_split ? 0u : (uint32_t)(kpart + 1));
                 }
             }
             }
@@ -360,7 +408,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             int64_t cbase = 0;
             int as = 0;
             uint32_t asph = 0;
-            for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch) {
+            for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += k_hi - k_lo) {
                 int nt, gi;
                 int64_t mt;
                 decode(t, nt, mt, gi);
@@ -368,9 +416,9 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 const int row0 = gi * g.kdim;
                 const int64_t sl = p.tps ? mt / p.tps : 0;
                 const int xs = p.tps ? (int)(mt - sl * p.tps) * G8_BM : 0;
-                for (int kc = 0; kc < nch; ++kc, as = as + 1 == p.astages ? 0 : as + 1,
+                for (int kc = k_lo; kc < k_hi; ++kc, as = as + 1 == p.astages ? 0 : as + 1,
                          asph ^= (as == 0 ? 1u : 0u)) {
-                    const int64_t cg = cbase + kc;
+                    const int64_t cg = cbase + (kc - k_lo);
                     ptx::mbar_wait(&as_empty[as], asph ^ 1);
                     if (leader) g8_cstamp(p, cg, 0);
                     if (leader && (p.debug & 2) && cg >= p.astages) {
@@ -391,14 +439,14 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
     } else if (warp == G8_TMA_WARP) {
         // ============================ weight TMA =========================================
         const uint32_t leader = ptx::elect_one();
-        const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
         int64_t sbase = 0;
         int s = 0;
         uint32_t ph = 0;
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, sbase += nstage) {
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
+            const int nstage = (k_hi - k_lo + Cfg::CPS - 1) / Cfg::CPS;
             const int row0 = gi * g.kpg + nt * BN + c_lo;  // (a part's rows start the stage)
             for (int kb = 0; kb < nstage; ++kb, s = s + 1 == p.bstages ? 0 : s + 1, ph ^= (s == 0 ? 1u : 0u)) {
                 const int64_t sg = sbase + kb;
@@ -408,8 +456,9 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 } else if (leader) {
                     uint8_t* st = smem + s * Cfg::STAGE_BYTES;
                     ptx::mbar_arrive_expect_tx(&b_full[s], Cfg::STAGE_BYTES);
-                    ptx::tma_load_2d(st, &tm_hi, &b_full[s], kb * Cfg::KE, row0);
-                    ptx::tma_load_2d(st + Cfg::B_BYTES, &tm_lo, &b_full[s], kb * Cfg::KE, row0);
+                    const int kx = k_lo * G8_CK + kb * Cfg::KE;
+                    ptx::tma_load_2d(st, &tm_hi, &b_full[s], kx, row0);
+                    ptx::tma_load_2d(st + Cfg::B_BYTES, &tm_lo, &b_full[s], kx, row0);
                 }
                 __syncwarp();
             }
@@ -420,22 +469,22 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
         constexpr uint32_t idesc_full = ptx::idesc_f32acc<BF16>(G8_BM, BN);
         const uint64_t db0 = ptx::sdesc_k_sw128(ptx::smem_u32(smem));
         constexpr uint32_t STG16 = Cfg::STAGE_BYTES >> 4, BLO16 = Cfg::B_BYTES >> 4;
-        const int nstage = (nch + Cfg::CPS - 1) / Cfg::CPS;
-        int64_t cbase = 0, sbase = 0;
+        int64_t cbase = 0;
         int slot = 0, s = 0;  // TMEM A ring slot and weight stage, with their phases
         uint32_t aph = 0, bph = 0;
         int i = 0;  // accumulator ranges issued so far (acc_empty phase)
         int li = 0;
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += nch, sbase += nstage, ++li) {
+        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, cbase += k_hi - k_lo, ++li) {
             int nt, gi;
             int64_t mt;
             decode(t, nt, mt, gi);
             const uint32_t idesc =
                 c_hi - c_lo == BN ? idesc_full : ptx::idesc_f32acc<BF16>(G8_BM, c_hi - c_lo);
             int kr = 0;  // position inside the accumulator range
-            for (int kc = 0; kc < nch; ++kc) {
+            for (int kc = k_lo; kc < k_hi; ++kc) {
+                const int j = kc - k_lo;  // chunk of this item (weight stages start at k_lo)
                 if (kr == 0) {  // a fresh accumulator range: the epilogue drained the last one
-                    if (kc > 0) {
+                    if (j > 0) {
                         if (leader) ptx::umma_commit(acc_full);
                         __syncwarp();
                         ++i;
@@ -443,16 +492,16 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                     ptx::mbar_wait(acc_empty, (i & 1) ^ 1);
                     ptx::tc_fence_after();
                 }
-                const int64_t cg = cbase + kc;
-                if (kc % Cfg::CPS == 0) ptx::mbar_wait(&b_full[s], bph);
+                const int64_t cg = cbase + j;
+                if (j % Cfg::CPS == 0) ptx::mbar_wait(&b_full[s], bph);
                 ptx::mbar_wait(&a_full[slot], aph);
                 ptx::tc_fence_after();
-                if (leader && kc == 0 && li < 5) g8_stamp(p, li * 6 + 2);
+                if (leader && j == 0 && li < 5) g8_stamp(p, li * 6 + 2);
                 if (leader) g8_cstamp(p, cg, 3);
                 if (leader) {
                     const uint32_t a_hi = tmem_base + BN + slot * Cfg::CHUNK_COLS;
                     const uint32_t a_lo = a_hi + Cfg::HALF_COLS;
-                    const uint64_t sb = db0 + (uint64_t)(s * STG16) + (kc % Cfg::CPS) * (G8_CK * Cfg::EB / 16);
+                    const uint64_t sb = db0 + (uint64_t)(s * STG16) + (j % Cfg::CPS) * (G8_CK * Cfg::EB / 16);
 #pragma unroll
                     for (int u = 0; u < G8_CK / Cfg::UK && !(p.debug & 4); ++u) {
                         const uint64_t dbh = sb + 2 * u, dbl = dbh + BLO16;
@@ -462,14 +511,14 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                         ptx::umma_ts<BF16>(tmem_base, a_hi + u * 8, dbh, idesc, 1u);
                     }
                     ptx::umma_commit(&a_empty[slot]);
-                    if (kc % Cfg::CPS == Cfg::CPS - 1 || kc == nch - 1) ptx::umma_commit(&b_empty[s]);
+                    if (j % Cfg::CPS == Cfg::CPS - 1 || kc == k_hi - 1) ptx::umma_commit(&b_empty[s]);
                 }
                 __syncwarp();
                 if (++slot == p.ring) {
                     slot = 0;
                     aph ^= 1;
                 }
-                if ((kc % Cfg::CPS == Cfg::CPS - 1 || kc == nch - 1) && ++s == p.bstages) {
+                if ((j % Cfg::CPS == Cfg::CPS - 1 || kc == k_hi - 1) && ++s == p.bstages) {
                     s = 0;
                     bph ^= 1;
                 }
@@ -569,6 +618,32 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
         if (r != CUDA_SUCCESS)
             return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string((int)r));
     }
+    if (prm.tail_k) {
+        // the K parts wait on each other: every CTA of the grid must be resident at once
+        int per_sm = 0;
+        const size_t smem_launch = std::max<size_t>(smem, 120 * 1024);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G8_THREADS, smem_launch) != cudaSuccess ||
+            (int64_t)per_sm * sm_count() < std::min<int64_t>(prm.items, sm_count())) {
+            (void)cudaGetLastError();
+            prm.items = prm.full_items + (prm.items - prm.full_items) / prm.tail_split;  // no split
+            prm.full_items = prm.items;
+            prm.tail_split = 1;
+            prm.tail_k = 0;
+        } else {
+            const int64_t tail_tiles = (prm.items - prm.full_items) / prm.tail_split;
+            const uint32_t need = (uint32_t)(tail_tiles * (BN / 32) * 4);
+            static std::mutex mu;
+            static uint32_t next = 0;
+            static uint32_t* pool = nullptr;
+            std::lock_guard<std::mutex> lk(mu);
+            if (!pool && cudaGetSymbolAddress(reinterpret_cast<void**>(&pool), g8_flags) != cudaSuccess)
+                return fail(CB_ERR_CUDA, "cudaGetSymbolAddress(g8_flags)");
+            if (need > (uint32_t)G8_FLAG_SLOTS) return fail(CB_ERR_UNSUPPORTED, "K8: too many tail tiles");
+            if (next + need > (uint32_t)G8_FLAG_SLOTS) next = 0;
+            prm.flags = pool + next;
+            next += need;
+        }
+    }
     const int grid = (int)std::min<int64_t>(prm.items, sm_count());
     if (std::getenv("CB_K8_TRACE")) prm.trace = debug_trace_buffer(1024, st);  // + chunk stamps
     kern<<<grid, G8_THREADS, std::max<size_t>(smem, 120 * 1024), st>>>(prm, mh, ml, ma);
@@ -614,7 +689,21 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
         const int64_t grid = std::min<int64_t>(prm.items, sm_count());
         const int64_t tail = prm.items % grid;
         static const bool no_split = std::getenv("CB_K8_NO_TAIL_SPLIT") != nullptr;
-        if (!no_split && prm.items > grid && tail > 0) {
+        // K split on request (CB_K8_KSPLIT = max parts, read per launch).  Measured on cfg4
+        // (3xBF16): the tail's MMAs drop from 31 to 14-21 us, but the parts' ordered
+        // read-add-store epilogues (~1.7 TB/s of NCHW stores chip-wide) give it all back:
+        // 94-98 us either way, so the channel split stays the default.
+        const char* ks = std::getenv("CB_K8_KSPLIT");
+        const int kmax = ks ? std::atoi(ks) : 0;
+        const int kparts = (int)std::min<int64_t>(std::min<int64_t>(grid / std::max<int64_t>(tail, 1), kmax),
+                                                  prm.nchunks / 4);
+        if (!no_split && prm.items > grid && tail > 0 && kparts >= 2 &&
+            (prm.nchunks + kparts - 1) / kparts <= prm.range_chunks) {
+            prm.full_items = prm.items - tail;
+            prm.tail_split = kparts;
+            prm.tail_k = 1;
+            prm.items = prm.full_items + tail * kparts;
+        } else if (!no_split && prm.items > grid && tail > 0) {
             // parts of 32+ channels that hold real output channels (a part past kpg would
             // have nothing to store)
             const int parts = (int)std::min<int64_t>(std::min<int64_t>(grid / tail, 4),

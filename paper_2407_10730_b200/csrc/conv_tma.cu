@@ -93,7 +93,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 __device__ __forceinline__ void trace_stamp(const TmaParams& p, int slot) {
-    if (p.trace && slot < TRACE_SLOTS) p.trace[blockIdx.x * TRACE_SLOTS + slot] = globaltimer();
+    if (kTrace && p.trace && slot < TRACE_SLOTS) p.trace[blockIdx.x * TRACE_SLOTS + slot] = globaltimer();
 }
 
 template <int BN, int STAGES, bool BF16, int CG>
@@ -1138,6 +1138,7 @@ int launch_fill_bias(int64_t images, int K, int PQ, const float* bias, float* y,
 static unsigned long long* g_trace = nullptr;
 static int g_trace_ctas = 0;
 unsigned long long* debug_trace_buffer(int ctas, cudaStream_t st) {
+    if (!kTrace) return nullptr;  // product build: no stamps, no buffer
     const size_t n = (size_t)1024 * TRACE_SLOTS;
     if (!g_trace && cudaMalloc(&g_trace, n * sizeof(unsigned long long)) != cudaSuccess)
         g_trace = nullptr;

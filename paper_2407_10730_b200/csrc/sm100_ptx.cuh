@@ -31,6 +31,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef CB_MBAR_HINT  // diagnostics: suspend up to CB_MBAR_HINT ns per try_wait
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(CB_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
@@ -40,6 +51,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)

@@ -329,13 +329,16 @@ K7_SHAPES = [(3, 7, 7), (3, 3, 3), (3, 5, 5), (4, 3, 3), (4, 7, 7), (2, 5, 3), (
 
 @pytest.mark.parametrize("crs", K7_SHAPES)
 @pytest.mark.parametrize("stride", [1, 2])
-@pytest.mark.parametrize("generic", [False, True, "no_pair"])
+@pytest.mark.parametrize("generic", [False, True, "no_pair", "no_planes"])
 def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
     from paper_2407_10730_b200.algos import conv_fused, fused_layout
     from paper_2407_10730_b200.descriptor import ConvDescriptor
     c, r, s = crs
     if generic == "no_pair":  # compile-time producers without the padded pair layout
         monkeypatch.setenv("CB_TS_NO_PAIR", "1")
+        generic = False
+    elif generic == "no_planes":  # pair layouts built from the fp32 window (no split planes)
+        monkeypatch.setenv("CB_TS_NO_PLANES", "1")
         generic = False
     elif generic:
         monkeypatch.setenv("CB_TS_GENERIC", "1")
@@ -463,3 +466,42 @@ def test_large_reductions_with_accumulator_promotion(cuda, key):
         errs[f"im2col/{v}"] = _check_conv(d, conv_baseline_im2col_gemm(inp, PhaseLedger(), variant=v), ref)
         errs[f"sconv/{v}"] = _check_conv(d, conv_main_blocked_direct(inp, PhaseLedger(), variant=v), ref)
     print(key, {k: f"{e:.1e}" for k, e in errs.items()})
+
+
+# K8's ragged last wave: cfg4-like shapes with more pixel tiles than SMs.  Both tails -- the
+# default channel split and the K split (CB_K8_KSPLIT: parts add into y in part order
+# through hand-off flags) -- must match the oracle and be bitwise reproducible.
+KSPLIT = [dict(batch=32, in_channels=64, in_h=28, in_w=28, out_channels=96, k_h=3, k_w=3,
+               pad_h=1, pad_w=1, has_bias=True),
+          dict(batch=40, in_channels=32, in_h=20, in_w=20, out_channels=256, k_h=5, k_w=5,
+               pad_h=2, pad_w=2, stride_h=1, stride_w=1)]
+
+
+@pytest.mark.parametrize("spec", range(len(KSPLIT)))
+def test_stepwise_tail_splits(cuda, spec, monkeypatch):
+    from paper_2407_10730_b200.algos import conv_baseline_im2col_gemm
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    from paper_2407_10730_b200.timing import PhaseLedger
+    d = ConvDescriptor(**KSPLIT[spec])
+    inp, (x, w, b) = _inputs(d)
+    ref = orc.conv_im2col64(d, x, w, b)
+    y0 = conv_baseline_im2col_gemm(inp, PhaseLedger())
+    _check_conv(d, y0, ref)
+    for parts in ("2", "3"):
+        monkeypatch.setenv("CB_K8_KSPLIT", parts)
+        y1 = conv_baseline_im2col_gemm(inp, PhaseLedger())
+        y2 = conv_baseline_im2col_gemm(inp, PhaseLedger())
+        _check_conv(d, y1, ref)
+        assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32)), "K-split tail not deterministic"
+
+
+def test_direct_conv_planes_bitwise(cuda, monkeypatch):
+    """K7's planes mode (window split once into bf16 planes) and the window-staged pair
+    producers feed the MMAs the same A values in the same order: bitwise-equal outputs."""
+    from paper_2407_10730_b200.algos import conv_fused
+    inp, (x, w, b) = _inputs(cfg("cfg3", batch=2))
+    y_planes = conv_fused(inp, variant="tc3xbf16")
+    monkeypatch.setenv("CB_TS_NO_PLANES", "1")
+    y_window = conv_fused(inp, variant="tc3xbf16")
+    assert np.array_equal(y_planes.view(np.uint32), y_window.view(np.uint32))
+    _check_conv(inp.desc, y_planes, orc.conv_direct_naive(inp.desc, x, w, b))

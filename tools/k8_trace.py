@@ -4,9 +4,11 @@
 Stamps (CB_K8_TRACE): per local item li < 5 of every CTA, producer warp 0 start / end, MMA
 first chunk / last commit, epilogue accumulator ready / last store; kernel start / end.
 """
-import ctypes, os, sys
+import ctypes, os, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2407_10730_b200.build import trace_lib  # noqa: E402
+os.environ.setdefault("CB_LIB_PATH", str(trace_lib()))  # the timelines exist only in this build
 os.environ["CB_K8_TRACE"] = "1"
 import numpy as np
 import torch

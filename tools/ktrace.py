@@ -13,6 +13,8 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2407_10730_b200.build import trace_lib  # noqa: E402
+os.environ.setdefault("CB_LIB_PATH", str(trace_lib()))  # the timelines exist only in this build
 os.environ.setdefault("CB_TMA_TRACE", "1")
 
 import numpy as np

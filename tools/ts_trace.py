@@ -5,9 +5,11 @@ Events: 0 TMA issue, 1/2/3/4 producer warp 0: window landed / A buffer free / A 
 st drained (11-14: the same for warp 8), 5/6 MMA: A full / accumulator free, 10 commit,
 7/8/9 epilogue: accumulator ready / released / last store issued, 15: kernel start.
 """
-import ctypes, os, sys
+import ctypes, os, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2407_10730_b200.build import trace_lib  # noqa: E402
+os.environ.setdefault("CB_LIB_PATH", str(trace_lib()))  # the timelines exist only in this build
 os.environ.setdefault("CB_TS_TRACE", "1")
 import numpy as np
 import torch
