@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <set>
 
 #include "cb_common.cuh"
 #include "sm100_ptx.cuh"
@@ -255,8 +256,22 @@ __device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_
 
 // compile-time reduction layouts (TsParams::fixed): 0 = generic offset-table producer
 #define CB_TS_FIXED_LIST(X) X(1, 3, 7, 7) X(2, 3, 3, 3) X(3, 3, 5, 5) X(4, 4, 3, 3) X(5, 4, 7, 7)
+template <int FX>
+struct TsLayout {
+    static constexpr int C = 0, R = 0, S = 0;
+};
+#define CB_TS_LAYOUT(id, c, r, s)          \
+    template <>                            \
+    struct TsLayout<id> {                  \
+        static constexpr int C = c, R = r, S = s; \
+    };
+CB_TS_FIXED_LIST(CB_TS_LAYOUT)
+#undef CB_TS_LAYOUT
 
-template <int CG>
+// One instantiation per (CTA group, compile-time layout FX, pair mode): each kernel holds
+// only its own unrolled producer -- with all layouts in one kernel the ncu profile showed
+// 12% of warp stalls as no_instructions (instruction-cache misses).
+template <int CG, int FX, bool PAIR>
 __global__ void __launch_bounds__(TS_THREADS, 1)
 conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUtensorMap tm_x,
                const __grid_constant__ CUtensorMap tm_whi, const __grid_constant__ CUtensorMap tm_wlo,
@@ -373,36 +388,25 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 2 : 12, i);
             const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
             const uint32_t a_lo = a_hi + half_cols;
-            if (p.fixed && !(p.debug & 16)) {
+            if (FX != 0 && !(p.debug & 16)) {
                 if (i < 2) {  // columns past the written groups: zero once per A buffer
                     const uint32_t z[4] = {0u, 0u, 0u, 0u};
-                    const int kd = p.pair ? g.C * g.R * (g.S + 1) : g.kdim;
+                    const int kd = PAIR ? g.C * g.R * (g.S + 1) : g.kdim;
                     for (int c4 = ((kd + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
                         ptx::tmem_st_32x32b_x4(a_hi + c4, z);
                         ptx::tmem_st_32x32b_x4(a_lo + c4, z);
                     }
                 }
                 const uint32_t cstride = 4u * p.box_rows * p.box_w, rstride = 4u * g.dh * p.box_w;
-                if (p.pair) {
+                using L = TsLayout<FX>;
+                if constexpr (FX != 0 && PAIR && L::S % 2 == 1) {
                     const uint32_t xs_pair = xs - 4u * p.pf;  // 8-byte aligned (plan_ts)
-                    switch (p.fixed) {
-#define CB_TS_CASE(id, c, r, s) \
-    case id: if (s % 2) build_pairs_part<c, r, s>(kpart, xs_pair, cstride, rstride, a_hi, a_lo); break;
-                        CB_TS_FIXED_LIST(CB_TS_CASE)
-#undef CB_TS_CASE
-                        default: break;
-                    }
-                } else {
-                    switch (p.fixed) {
-#define CB_TS_CASE(id, c, r, s) \
-    case id: build_fixed_part<c, r, s>(kpart, xs, cstride, rstride, a_hi, a_lo, swap); break;
-                        CB_TS_FIXED_LIST(CB_TS_CASE)
-#undef CB_TS_CASE
-                        default: break;
-                    }
+                    build_pairs_part<L::C, L::R, L::S>(kpart, xs_pair, cstride, rstride, a_hi, a_lo);
+                } else if constexpr (FX != 0 && !PAIR) {
+                    build_fixed_part<L::C, L::R, L::S>(kpart, xs, cstride, rstride, a_hi, a_lo, swap);
                 }
             }
-            for (int kc = kpart; kc < nchunks && !p.fixed && !(p.debug & 16); kc += KPARTS) {
+            for (int kc = kpart; kc < nchunks && FX == 0 && !(p.debug & 16); kc += KPARTS) {
                 const uint32_t ko = ptx::smem_u32(koff + kc * 32);
                 uint32_t hv[16], lv[16];
 #pragma unroll
@@ -609,332 +613,21 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
 }
 
 // ----------------------------------------------------------------------------------------
-// K7 planes mode (pair layouts, one CTA per tile): the (hi, lo) split is done once per input
-// element instead of once per A element.  The ncu source view of the window-staged kernel
-// above had its A build issue-bound (~7 instructions per k pair: LDS.64, two bf16x2
-// conversions, the residual subtractions) at ~1700 of ~2400 cycles a tile; a window element
-// feeds ~3.5 A elements on cfg3, so here:
-//   * warps 8-15 (two groups of four, alternating tiles) load the tile's input window
-//     straight from global memory (float4, zero outside the image), split it and store two
-//     bf16 planes [C][rows][box_w] (hi and lo) into a 3-slot ring;
-//   * warps 0-7 (two per TMEM lane quadrant) build A from the planes: every k pair is one
-//     LDS.32 per plane -- already the packed bf16x2 TMEM word -- then tcgen05.st;
-//   * warps 16-19 epilogue, 20 weight TMA, 21 MMA, as in the kernel above.
-// ----------------------------------------------------------------------------------------
-constexpr int TSP_BUILD_WARPS = 8;
-constexpr int TSP_SPLIT_WARP0 = 8;
-constexpr int TSP_EPI_WARP0 = 16;
-constexpr int TSP_TMA_WARP = 20;
-constexpr int TSP_MMA_WARP = 21;
-constexpr int TSP_THREADS = 22 * 32;
-constexpr int TSP_NSP = 3;  // plane slots
-
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-
-// groups [G0, G1) of 8 elements of the padded pair layout: per pair one word from each plane
-template <int C, int R, int S, int G0, int G1>
-__device__ __forceinline__ void build_from_planes(uint32_t hb, uint32_t lb, uint32_t cstride,
-                                                  uint32_t rstride, uint32_t a_hi, uint32_t a_lo) {
-    constexpr int SP = S + 1, KD = C * R * SP, NG = G1 - G0, D = 2;
-    uint32_t h[D + 1][4], l[D + 1][4];
-#pragma unroll
-    for (int step = 0; step < NG + D; ++step) {
-        if (step < NG) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k = (G0 + step) * 8 + 2 * e;
-                if (k < KD) {
-                    const int cr = k / SP, sp = k % SP;
-                    const uint32_t off = (cr / R) * cstride + (cr % R) * rstride + 2 * sp;
-                    h[step % (D + 1)][e] = lds_u32(hb + off);
-                    l[step % (D + 1)][e] = lds_u32(lb + off);
-                } else {
-                    h[step % (D + 1)][e] = 0u;
-                    l[step % (D + 1)][e] = 0u;
-                }
-            }
-        }
-        if (step >= D) {
-            const int gi = step - D;
-            ptx::tmem_st_32x32b_x4(a_hi + (G0 + gi) * 4, h[gi % (D + 1)]);
-            ptx::tmem_st_32x32b_x4(a_lo + (G0 + gi) * 4, l[gi % (D + 1)]);
-        }
-    }
-}
-
-template <int C, int R, int S>
-__device__ __forceinline__ void build_from_planes_part(int kpart, uint32_t hb, uint32_t lb, uint32_t cstride,
-                                                       uint32_t rstride, uint32_t a_hi, uint32_t a_lo) {
-    constexpr int G = (C * R * (S + 1) + 7) / 8, G1 = (G + 1) / 2;
-    if (kpart == 0)
-        build_from_planes<C, R, S, 0, G1>(hb, lb, cstride, rstride, a_hi, a_lo);
-    else
-        build_from_planes<C, R, S, G1, G>(hb, lb, cstride, rstride, a_hi, a_lo);
-}
-
-__global__ void __launch_bounds__(TSP_THREADS, 1)
-conv_tsp_kernel(const __grid_constant__ TsParams p, const float* __restrict__ x,
-                const __grid_constant__ CUtensorMap tm_whi, const __grid_constant__ CUtensorMap tm_wlo,
-                const __grid_constant__ CUtensorMap tm_y) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint8_t* w_hi = smem;
-    uint8_t* w_lo = smem + p.w_half_bytes;
-    // plane slot s: hi plane at planes + s * stage_stride, lo plane half a slot later
-    uint8_t* planes = smem + 2 * p.w_half_bytes;
-    const uint32_t plane_half = p.stage_stride / 2;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(planes + TSP_NSP * p.stage_stride);
-    uint64_t* w_full = bars;            // 1
-    uint64_t* p_full = bars + 1;        // 3: planes of the slot written
-    uint64_t* p_empty = bars + 4;       // 3: builders done with the slot
-    uint64_t* a_full = bars + 7;        // 2
-    uint64_t* a_empty = bars + 9;       // 2
-    uint64_t* acc_full = bars + 11;     // 2
-    uint64_t* acc_empty = bars + 13;    // 2
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-    float* ostage = reinterpret_cast<float*>(planes + TSP_NSP * p.stage_stride + 1024);
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const Geom& g = p.g;
-    const int col_a0 = 2 * p.n_pad;  // TMEM: [acc0 | acc1 | A0 (hi, lo) | A1 (hi, lo)]
-    const int half_cols = p.kp / 2;
-
-    if (threadIdx.x == 0) {
-        ptx::mbar_init(w_full, 1);
-        for (int b = 0; b < TSP_NSP; ++b) {
-            ptx::mbar_init(&p_full[b], 128);
-            ptx::mbar_init(&p_empty[b], 32 * TSP_BUILD_WARPS);
-        }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&a_full[b], 32 * TSP_BUILD_WARPS);
-            ptx::mbar_init(&a_empty[b], 1);
-            ptx::mbar_init(&acc_full[b], 1);
-            ptx::mbar_init(&acc_empty[b], 128);
-        }
-        ptx::fence_mbar_init();
-    }
-    if (warp == TSP_TMA_WARP && lane == 0) {
-        ptx::tma_prefetch_desc(&tm_whi);
-        ptx::tma_prefetch_desc(&tm_wlo);
-    }
-    if (warp == TSP_MMA_WARP) ptx::tmem_alloc(tmem_slot, TS_TMEM_COLS);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    const int unit0 = (int)blockIdx.x, nunits = (int)gridDim.x;
-
-    if (warp < TSP_BUILD_WARPS) {
-        // ============================ A builders =======================================
-        const int quad = warp & 3, kpart = warp >> 2;
-        const int m = quad * 32 + lane;
-        const uint32_t lane_addr = tmem_base + ((uint32_t)(quad * 32) << 16);
-        const uint32_t cstride = 2u * p.box_rows * p.box_w, rstride = 2u * g.dh * p.box_w;
-        const uint32_t planes_u32 = ptx::smem_u32(planes);
-        int i = 0, sp = 0;
-        uint32_t sph = 0;
-        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
-            const int b = i & 1;
-            const uint32_t ph = (i >> 1) & 1;
-            const int p0 = min(tw.ti * TS_BM, g.PQ - 1);
-            const int oy_a = div_q(p0, p);
-            const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
-            const int oy = div_q(pix, p);
-            const int ox = pix - oy * g.Q;
-            // pair base element: the pad-tap shift pf keeps every k pair one aligned word
-            const uint32_t base = 2u * (uint32_t)((oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw) - p.pf);
-            ptx::mbar_wait(&p_full[sp], sph);
-            ptx::mbar_wait(&a_empty[b], ph ^ 1);
-            ptx::tc_fence_after();
-            const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
-            const uint32_t a_lo = a_hi + half_cols;
-            if (i < 2) {  // columns past the written groups: zero once per A buffer
-                const uint32_t z[4] = {0u, 0u, 0u, 0u};
-                const int kd = g.C * g.R * (g.S + 1);
-                for (int c4 = ((kd + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 8) {
-                    ptx::tmem_st_32x32b_x4(a_hi + c4, z);
-                    ptx::tmem_st_32x32b_x4(a_lo + c4, z);
-                }
-            }
-            const uint32_t hb = planes_u32 + sp * p.stage_stride + base;
-            const uint32_t lb = hb + plane_half;
-            switch (p.fixed) {
-#define CB_TSP_CASE(id, c, r, s) \
-    case id: if (s % 2) build_from_planes_part<c, r, s>(kpart, hb, lb, cstride, rstride, a_hi, a_lo); break;
-                CB_TS_FIXED_LIST(CB_TSP_CASE)
-#undef CB_TSP_CASE
-                default: break;
-            }
-            ptx::tmem_st_wait();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&a_full[b]);
-            ptx::mbar_arrive(&p_empty[sp]);
-            if (++sp == TSP_NSP) {
-                sp = 0;
-                sph ^= 1;
-            }
-        }
-    } else if (warp < TSP_EPI_WARP0) {
-        // ============================ window loaders / splitters =======================
-        const int grp = (warp - TSP_SPLIT_WARP0) >> 2;
-        const int st = ((warp - TSP_SPLIT_WARP0) & 3) * 32 + lane;
-        const int wq = p.box_w / 4;                   // float4s per window row
-        const int n4 = g.C * p.box_rows * wq;         // float4s per window
-        const float inv_wq = 1.0f / (float)wq;
-        const uint32_t planes_u32 = ptx::smem_u32(planes);
-        int i = 0;
-        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
-            if ((i & 1) != grp) continue;
-            const int sp = i % TSP_NSP;
-            const uint32_t sph = (uint32_t)((i / TSP_NSP) & 1);
-            const int n = tw.n;
-            const int p0 = min(tw.ti * TS_BM, g.PQ - 1);
-            const int iy0 = div_q(p0, p) * g.sh - g.ph;
-            const float* xn = x + (int64_t)n * g.C * g.HW;
-            ptx::mbar_wait(&p_empty[sp], sph ^ 1);
-            const uint32_t hb = planes_u32 + sp * p.stage_stride;
-            // batches of 8 float4 loads in flight per thread
-            for (int j0 = st; j0 < n4; j0 += 128 * 8) {
-                float4 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j = j0 + u * 128;
-                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (j < n4) {
-                        const int cr = __float2int_rz(((float)j + 0.5f) * inv_wq);
-                        const int j4 = j - cr * wq;
-                        const int c = cr / p.box_rows, r = cr - (cr / p.box_rows) * p.box_rows;
-                        const int iy = iy0 + r, ix = 4 * j4 - p.x0;
-                        if ((unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W)
-                            v[u] = __ldg(reinterpret_cast<const float4*>(xn + ((int64_t)c * g.H + iy) * g.W + ix));
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j = j0 + u * 128;
-                    if (j < n4) {
-                        uint32_t h0, l0, h1, l1;
-                        split_pair(v[u].x, v[u].y, h0, l0);
-                        split_pair(v[u].z, v[u].w, h1, l1);
-                        const uint32_t a = hb + 8u * (uint32_t)j;  // 4 bf16 per float4
-                        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(h0), "r"(h1) : "memory");
-                        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a + plane_half), "r"(l0), "r"(l1)
-                                     : "memory");
-                    }
-                }
-            }
-            ptx::mbar_arrive(&p_full[sp]);
-        }
-    } else if (warp < TSP_TMA_WARP) {
-        // ============================ epilogue ==========================================
-        const int quad = warp & 3;
-        const int m = quad * 32 + lane;
-        const bool issuer = threadIdx.x == TSP_EPI_WARP0 * 32;
-        int i = 0, chunk = 0;
-        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
-            const int b = i & 1;
-            const uint32_t ph = (i >> 1) & 1;
-            const int n = tw.n;
-            const int p0 = tw.ti * TS_BM;
-            const int pix = p0 + m;
-            const bool valid = pix < g.PQ;
-            float* dst = p.out + (int64_t)n * g.K * g.PQ + pix;
-            ptx::mbar_wait(&acc_full[b], ph);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int c0 = 0; c0 < g.K; c0 += 32, ++chunk) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + b * p.n_pad + c0, r);
-                ptx::tmem_ld_wait();
-                if (c0 + 32 >= g.K) {  // accumulator fully in registers: release it early
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(&acc_empty[b]);
-                }
-                if (p.tma_store) {
-                    float* buf = ostage + (chunk & 1) * (32 * TS_BM);
-                    if (issuer) ptx::bulk_wait_read<1>();  // the store 2 chunks ago left buf
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    const uint32_t bs = ptx::smem_u32(buf + m);
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        sts_f32(bs + 4 * e * TS_BM, __uint_as_float(r[e]) +
-                                                        (p.bias && c0 + e < g.K ? __ldg(p.bias + c0 + e) : 0.f));
-                    ptx::fence_proxy_async_smem();
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (issuer && p0 < g.PQ) {
-                        ptx::tma_store_3d(&tm_y, buf, p0, c0, n);
-                        ptx::bulk_commit();
-                    }
-                } else if (valid) {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int co = c0 + e;
-                        if (co < g.K) dst[(int64_t)co * g.PQ] = __uint_as_float(r[e]) + (p.bias ? __ldg(p.bias + co) : 0.f);
-                    }
-                }
-            }
-        }
-        if (issuer) ptx::bulk_wait_all();
-    } else if (warp == TSP_TMA_WARP) {
-        // ============================ weights, once =====================================
-        if (ptx::elect_one()) {
-            ptx::mbar_arrive_expect_tx(w_full, 2 * p.w_half_bytes);
-            for (int kb = 0; kb < p.kb_w / 64; ++kb) {
-                ptx::tma_load_2d(w_hi + (size_t)kb * p.w_rows * 128, &tm_whi, w_full, kb * 64, 0);
-                ptx::tma_load_2d(w_lo + (size_t)kb * p.w_rows * 128, &tm_wlo, w_full, kb * 64, 0);
-            }
-        }
-        __syncwarp();
-    } else {
-        // ============================ MMA issuer ========================================
-        const uint32_t leader = ptx::elect_one();
-        const uint32_t idesc = ptx::idesc_f32acc<true>(TS_BM, p.n_pad);
-        const uint64_t dbh0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_hi));
-        const uint64_t dbl0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_lo));
-        const uint32_t blk16 = (uint32_t)(p.w_rows * 128) >> 4;  // one 64-wide K block of B
-        const int ksteps = p.kp / 16;
-        ptx::mbar_wait(w_full, 0);
-        int i = 0;
-        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
-            const int b = i & 1;
-            const uint32_t ph = (i >> 1) & 1;
-            ptx::mbar_wait(&a_full[b], ph);
-            ptx::mbar_wait(&acc_empty[b], ph ^ 1);
-            ptx::tc_fence_after();
-            const uint32_t d = tmem_base + b * p.n_pad;
-            const uint32_t a_hi = tmem_base + col_a0 + b * p.kp;
-            const uint32_t a_lo = a_hi + half_cols;
-            if (leader) {
-                for (int j = 0; j < ksteps; ++j) {
-                    const uint64_t boff = (uint64_t)((j >> 2) * blk16 + (j & 3) * 2);
-                    ptx::umma_ts_bf16(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
-                    ptx::umma_ts_bf16(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
-                    ptx::umma_ts_bf16(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
-                }
-                ptx::umma_commit(&a_empty[b]);
-                ptx::umma_commit(&acc_full[b]);
-            }
-            __syncwarp();
-        }
-    }
-
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == TSP_MMA_WARP) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, TS_TMEM_COLS);
-    }
-}
-
-// ----------------------------------------------------------------------------------------
 // Host side
 // ----------------------------------------------------------------------------------------
+using TsKernel = void (*)(const TsParams, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                         const CUtensorMap);
+template <int CG>
+static TsKernel ts_kernel_for(int fixed, bool pair) {
+    switch (fixed) {
+#define CB_TS_K(id, c, r, s) \
+    case id: return pair ? conv_ts_kernel<CG, id, true> : conv_ts_kernel<CG, id, false>;
+        CB_TS_FIXED_LIST(CB_TS_K)
+#undef CB_TS_K
+        default: return conv_ts_kernel<CG, 0, false>;
+    }
+}
+
 struct TsPlan {
     bool ok;
     int cg;  // 1: one CTA per 128-pixel tile; 2: CTA pairs (cta_group::2) on 256-pixel tiles
@@ -1125,32 +818,19 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.w_rows = pl.n_pad / pl.cg;
     if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
     if (std::getenv("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(conv_ts_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        227 * 1024);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(conv_ts_kernel<2>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    });
-    if (attr_err != cudaSuccess)
-        return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-    const int units = (int)std::min<int64_t>(prm.total_tiles, sm_count() / pl.cg);
-    // planes mode (pair layouts, single CTAs): window loaded and split once per tile
-    const size_t planes_smem = 1024 + 2 * (size_t)pl.w_half_bytes + TSP_NSP * (size_t)pl.stage_stride +
-                               1024 + 2 * 32 * TS_BM * 4;
-    if (pl.pair && pl.cg == 1 && prm.fixed && planes_smem <= 227 * 1024 && !std::getenv("CB_TS_NO_PLANES")) {
-        static std::once_flag once_p;
-        static cudaError_t attr_p = cudaSuccess;
-        std::call_once(once_p, [] {
-            attr_p = cudaFuncSetAttribute(conv_tsp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        });
-        if (attr_p != cudaSuccess)
-            return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_p));
-        conv_tsp_kernel<<<units, TSP_THREADS, planes_smem, st>>>(prm, x, mwh, mwl, my);
-        return check_launch("conv_tsp_kernel");
+    const TsKernel kern = pl.cg == 2 ? ts_kernel_for<2>(prm.fixed, pl.pair) : ts_kernel_for<1>(prm.fixed, pl.pair);
+    {
+        static std::mutex mu;
+        static std::set<const void*> ready;  // kernels whose smem attribute is set
+        std::lock_guard<std::mutex> lk(mu);
+        if (!ready.count(reinterpret_cast<const void*>(kern))) {
+            const cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            if (attr_err != cudaSuccess)
+                return fail(CB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+            ready.insert(reinterpret_cast<const void*>(kern));
+        }
     }
+    const int units = (int)std::min<int64_t>(prm.total_tiles, sm_count() / pl.cg);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(units * pl.cg));
     cfg.blockDim = dim3(TS_THREADS);
@@ -1163,8 +843,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pl.cg == 2 ? 1 : 0;  // no cluster attribute for single CTAs
-    cudaError_t e = pl.cg == 2 ? cudaLaunchKernelEx(&cfg, conv_ts_kernel<2>, prm, mx, mwh, mwl, my)
-                               : cudaLaunchKernelEx(&cfg, conv_ts_kernel<1>, prm, mx, mwh, mwl, my);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mx, mwh, mwl, my);
     if (e != cudaSuccess) return fail(CB_ERR_CUDA, std::string("conv_ts launch: ") + cudaGetErrorString(e));
     return check_launch("conv_ts_kernel");
 }

@@ -329,16 +329,13 @@ K7_SHAPES = [(3, 7, 7), (3, 3, 3), (3, 5, 5), (4, 3, 3), (4, 7, 7), (2, 5, 3), (
 
 @pytest.mark.parametrize("crs", K7_SHAPES)
 @pytest.mark.parametrize("stride", [1, 2])
-@pytest.mark.parametrize("generic", [False, True, "no_pair", "no_planes"])
+@pytest.mark.parametrize("generic", [False, True, "no_pair"])
 def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
     from paper_2407_10730_b200.algos import conv_fused, fused_layout
     from paper_2407_10730_b200.descriptor import ConvDescriptor
     c, r, s = crs
     if generic == "no_pair":  # compile-time producers without the padded pair layout
         monkeypatch.setenv("CB_TS_NO_PAIR", "1")
-        generic = False
-    elif generic == "no_planes":  # pair layouts built from the fp32 window (no split planes)
-        monkeypatch.setenv("CB_TS_NO_PLANES", "1")
         generic = False
     elif generic:
         monkeypatch.setenv("CB_TS_GENERIC", "1")
@@ -494,14 +491,3 @@ def test_stepwise_tail_splits(cuda, spec, monkeypatch):
         _check_conv(d, y1, ref)
         assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32)), "K-split tail not deterministic"
 
-
-def test_direct_conv_planes_bitwise(cuda, monkeypatch):
-    """K7's planes mode (window split once into bf16 planes) and the window-staged pair
-    producers feed the MMAs the same A values in the same order: bitwise-equal outputs."""
-    from paper_2407_10730_b200.algos import conv_fused
-    inp, (x, w, b) = _inputs(cfg("cfg3", batch=2))
-    y_planes = conv_fused(inp, variant="tc3xbf16")
-    monkeypatch.setenv("CB_TS_NO_PLANES", "1")
-    y_window = conv_fused(inp, variant="tc3xbf16")
-    assert np.array_equal(y_planes.view(np.uint32), y_window.view(np.uint32))
-    _check_conv(inp.desc, y_planes, orc.conv_direct_naive(inp.desc, x, w, b))
