@@ -1,0 +1,6 @@
+set -o pipefail
+mkdir -p gpurun_out/r2z
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "activation_split or baseline_configs or fused_matches or every_tile" > gpurun_out/r2z/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/r2z/pytest.log
+for env in "CB_K0_ROWS=1" "CB_X=0" "CB_K0_ROWS=1" "CB_X=0"; do echo "== $env"; env $env CB_KT_COLD=1 timeout 120 python tools/ktime.py cfg4 2>&1 | tail -1; done > gpurun_out/r2z/k0.log 2>&1; cat gpurun_out/r2z/k0.log
+for env in "CB_K0_ROWS=1" "CB_X=0" "CB_K0_ROWS=1" "CB_X=0"; do env $env timeout 300 python bench.py --no-breakdown --no-cpu-baseline --no-variants 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().splitlines()[-1]);print('$env',round(d['value']),d['ms_per_step'],d['step_phases_us'])"; done
+timeout 300 ncu --kernel-name regex:"act_split" --launch-skip 5 --launch-count 1 --clock-control none --set full -o gpurun_out/r2z/k0q -f python tools/ktime.py cfg4 > /dev/null 2>&1; echo "ncu rc=$?"
