@@ -37,6 +37,7 @@ constexpr int G8_ASTAGES_MAX = 8;
 constexpr int G8_ASTAGE_BYTES = 32 * G8_BM * 4;  // [32 k][128 px] fp32
 constexpr int G8_TMEM_COLS = 512;
 constexpr int G8_CK = 32;  // reduction elements per A chunk
+constexpr int G8_OSTAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: [32 channels][32 pixels] fp32
 
 struct G8Params {
     Geom g;
@@ -76,6 +77,11 @@ struct G8Params {
     unsigned long long* trace;  // diagnostics (CB_K8_TRACE): per-CTA globaltimer stamps
     int astages;                // A chunk stages in smem (TMA sources)
     int debug;                  // diagnostics (CB_K8_DEBUG): 1 no weight TMA, 2 no A TMA, 4 no MMA, 8 no A build, 16 no epilogue stores, 32 no bias
+    // TMA-store epilogue (tma_y = 1: NCHW y as {PQ, K, N}; 2: slice accumulators as {np, K,
+    // slices}): an epilogue warp stages its 32 rows x 32 channels in smem and one lane
+    // stores them with the TMA engine; warps whose rows cross an image or hold invalid rows,
+    // partial channel chunks and read-add-write ranges use per-lane stores
+    int tma_y;
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* f) {
@@ -134,7 +140,8 @@ struct G8Cfg {
 template <int BN, bool BF16>
 __global__ void __launch_bounds__(G8_THREADS, 1)
 gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUtensorMap tm_hi,
-               const __grid_constant__ CUtensorMap tm_lo, const __grid_constant__ CUtensorMap tm_a) {
+               const __grid_constant__ CUtensorMap tm_lo, const __grid_constant__ CUtensorMap tm_a,
+               const __grid_constant__ CUtensorMap tm_y) {
     using Cfg = G8Cfg<BN, BF16>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -151,6 +158,9 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
     uint64_t* as_full = acc_empty + 1;          // [astages]
     uint64_t* as_empty = as_full + p.astages;   // [astages]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(as_empty + p.astages);
+    // epilogue staging, one 4 KB buffer per epilogue warp (1 KB after the barriers)
+    float* ostage = reinterpret_cast<float*>(smem + p.bstages * Cfg::STAGE_BYTES +
+                                             p.astages * G8_ASTAGE_BYTES + 1024);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -369,21 +379,69 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 }
                 uint32_t* flag = kord ? p.flags + ((size_t)(ktau * (BN / 32) + c0 / 32) * 4 + quad) : nullptr;
                 if (kord && kpart > 0) {  // the previous part's rows of this chunk are stored
-                    if (lane == 0)
+                    if (lane == 0) {
                         while (ld_acquire_gpu(flag) != (uint32_t)kpart) __nanosleep(64);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");  // before a TMA add
+                    }
                     __syncwarp();
                 }
-                if (jvalid && !(p.debug & 16)) {
                 const int nvalid = min(32, ncol - c0);
                 const int fb = gi * g.kpg + f_tile0 + c0;
-                float* dst = p.out + obase + (int64_t)fb * ostride;
-                if (add) {  // all loads before the first store (no per-element round trips)
-                    float o[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = e < nvalid ? __ldcg(dst + (int64_t)e * ostride) : 0.f;
+                // TMA store (or TMA add for later ranges / K parts / add_mode) of this warp's
+                // 32 x 32 block: every row valid and in one image (NCHW) / slice, a whole
+                // channel chunk
+                bool tma_ok = p.tma_y && nvalid == 32 && !(p.debug & 16) && __all_sync(0xffffffffu, jvalid);
+                int32_t yc0 = 0, yc2 = 0;
+                if (tma_ok) {
+                    const int64_t ja = p.pm.j_begin + jl;
+                    if (p.tma_y == 1) {
+                        const int64_t n = ja / g.PQ;
+                        yc0 = (int32_t)(ja - n * g.PQ);
+                        yc2 = (int32_t)n;
+                    } else {  // slice-aligned tile: slice mt / tps, pixel offset within it
+                        const int64_t sl = mt / p.tps;
+                        yc0 = (int32_t)((mt - sl * p.tps) * G8_BM + m);
+                        yc2 = (int32_t)sl;
+                    }
+                    const int32_t y2_0 = __shfl_sync(0xffffffffu, yc2, 0);
+                    tma_ok = __all_sync(0xffffffffu, y2_0 == yc2);  // one image / slice
+                    yc0 = __shfl_sync(0xffffffffu, yc0, 0);
+                    yc2 = y2_0;
+                }
+                if (tma_ok) {
+                    float* buf = ostage + (warp - G8_EPI_WARP0) * (G8_OSTAGE_BYTES / 4);
+                    if (lane == 0) ptx::bulk_wait_read<0>();  // this warp's previous store left buf
+                    __syncwarp();
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
-                        if (e < nvalid) dst[(int64_t)e * ostride] = __uint_as_float(r[e]) + o[e];
+                        buf[e * 32 + lane] = __uint_as_float(r[e]) +
+                                             (!add && p.bias && !(p.debug & 32) ? __ldg(p.bias + fb + e) : 0.f);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (add) {
+                            // a later range of this CTA adds onto its own earlier store of the
+                            // chunk: make sure that store has landed
+                            if (!kord) ptx::bulk_wait_all();
+                            ptx::tma_reduce_add_3d(&tm_y, buf, yc0, fb, yc2);
+                        } else {
+                            ptx::tma_store_3d(&tm_y, buf, yc0, fb, yc2);
+                        }
+                        ptx::bulk_commit();
+                    }
+                } else if (jvalid && !(p.debug & 16)) {
+                float* dst = p.out + obase + (int64_t)fb * ostride;
+                if (add) {  // all loads of a half before its first store (no per-element round trips)
+#pragma unroll
+                    for (int h = 0; h < 32; h += 16) {
+                        float o[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            o[e] = h + e < nvalid ? __ldcg(dst + (int64_t)(h + e) * ostride) : 0.f;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (h + e < nvalid) dst[(int64_t)(h + e) * ostride] = __uint_as_float(r[h + e]) + o[e];
+                    }
                 } else {
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
@@ -393,6 +451,10 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 }
                 }
                 if (kord) {  // hand the chunk on to the next part (the last one resets the flag)
+                    if (tma_ok && lane == 0) {  // the TMA store / add has landed in global memory
+                        ptx::bulk_wait_all();
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
                     __threadfence();
                     __syncwarp();
                     if (lane == 0) st_release_gpu(flag, kpart + 1 == p.tail_split ? 0u : (uint32_t)(kpart + 1));
@@ -401,6 +463,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
             }
             if (threadIdx.x == G8_EPI_WARP0 * 32 && li < 5) g8_stamp(p, li * 6 + 5);
         }
+        if (lane == 0 && p.tma_y) ptx::bulk_wait_all();
     } else if (warp == G8_ATMA_WARP) {
         // ============================ A chunks by TMA (matrix sources) ==================
         if (p.tma_a) {
@@ -564,12 +627,15 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
     prm.astages = 4;
     if (const char* e = std::getenv("CB_K8_ASTAGES"))  // even: each stage stays with one producer group
         prm.astages = std::max(2, std::min(G8_ASTAGES_MAX, std::atoi(e))) & ~1;
-    prm.bstages = std::min(8, (225 * 1024 - prm.astages * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
+    const int ostage_bytes = 1024 + 8 * G8_OSTAGE_BYTES;  // barriers' KB + epilogue staging
+    prm.bstages = std::min(8, (225 * 1024 - ostage_bytes - prm.astages * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
     if (const char* e = std::getenv("CB_K8_DEBUG")) prm.debug = std::atoi(e);
     if (const char* e = std::getenv("CB_K8_BSTAGES")) prm.bstages = std::max(2, std::min(prm.bstages, std::atoi(e)));
     if (prm.bstages < 2) return fail(CB_ERR_UNSUPPORTED, "K8: shared memory for 2 weight stages");
+    if (8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * prm.astages) > 1024)
+        return fail(CB_ERR_UNSUPPORTED, "K8: barrier block overflow");
     const size_t smem = 1024 + (size_t)prm.bstages * Cfg::STAGE_BYTES + prm.astages * G8_ASTAGE_BYTES +
-                        8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * prm.astages);
+                        ostage_bytes;
     auto kern = gemm_ts_kernel<BN, BF16>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -644,9 +710,23 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
             next += need;
         }
     }
+    CUtensorMap my{};
+    if (prm.tma_y) {  // NCHW y {PQ, K, N} or slice accumulators {np, K, slices}, 32 x 32 boxes
+        const bool nchw = prm.tma_y == 1;
+        const cuuint64_t inner = nchw ? (cuuint64_t)prm.g.PQ : (cuuint64_t)prm.np;
+        const cuuint64_t outer = nchw ? (cuuint64_t)prm.g.N : (cuuint64_t)(prm.pm.j_count / prm.np);
+        cuuint64_t dims[3] = {inner, (cuuint64_t)prm.g.K, outer};
+        cuuint64_t strides[2] = {inner * 4, inner * prm.g.K * 4};
+        cuuint32_t box[3] = {32, 32, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = enc(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, prm.out, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) prm.tma_y = 0;  // per-lane stores
+    }
     const int grid = (int)std::min<int64_t>(prm.items, sm_count());
     if (std::getenv("CB_K8_TRACE")) prm.trace = debug_trace_buffer(1024, st);  // + chunk stamps
-    kern<<<grid, G8_THREADS, std::max<size_t>(smem, 120 * 1024), st>>>(prm, mh, ml, ma);
+    kern<<<grid, G8_THREADS, std::max<size_t>(smem, 120 * 1024), st>>>(prm, mh, ml, ma, my);
     return check_launch("gemm_ts_kernel");
 }
 
@@ -725,6 +805,15 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
         prm.tma_a = 1;
         prm.np = np;
         prm.tps = (np + G8_BM - 1) / G8_BM;
+    }
+    // TMA-store epilogue: NCHW y (the Im2col-GEMM drop-in) or equal slice-aligned accumulators
+    // (SConv); 16-byte row strides and base
+    prm.tma_y = 0;
+    if (!std::getenv("CB_K8_NO_TMA_STORE") && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !add_mode) {
+        if (pm.dst_mode == DST_NCHW && g.PQ % 4 == 0 && pm.j_begin == 0)
+            prm.tma_y = 1;
+        else if (pm.dst_mode == DST_SLICES && prm.tps && prm.np % 4 == 0)
+            prm.tma_y = 2;
     }
     switch (bn) {
         case 64: return bf16 ? launch_g8_cfg<64, true>(prm, w_hi, w_lo, st) : launch_g8_cfg<64, false>(prm, w_hi, w_lo, st);

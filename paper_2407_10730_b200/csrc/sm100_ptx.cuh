@@ -102,6 +102,15 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
         "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
         : "memory");
 }
+// smem -> global element-wise fp32 add (the TMA unit reads, adds and writes in L2)
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int32_t c0,
+                                                  int32_t c1, int32_t c2) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+        : "memory");
+}
 // 1-D bulk copy smem -> global (bytes a multiple of 16, both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_store_1d(void* gdst, const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),

@@ -8,8 +8,11 @@ st drained (11-14: the same for warp 8), 5/6 MMA: A full / accumulator free, 10 
 import ctypes, os, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+# the timelines exist only in the diagnostics build: point the loader at it before the
+# package is imported, then (re)build it if it is missing or stale
+os.environ.setdefault("CB_LIB_PATH", str(Path(__file__).resolve().parent.parent / "_ab" / "libconvb200_trace.so"))
 from paper_2407_10730_b200.build import trace_lib  # noqa: E402
-os.environ.setdefault("CB_LIB_PATH", str(trace_lib()))  # the timelines exist only in this build
+trace_lib()
 os.environ.setdefault("CB_TS_TRACE", "1")
 import numpy as np
 import torch
