@@ -491,3 +491,21 @@ def test_stepwise_tail_splits(cuda, spec, monkeypatch):
         _check_conv(d, y1, ref)
         assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32)), "K-split tail not deterministic"
 
+
+
+@pytest.mark.parametrize("mode", ["CB_TMA_WSTORE", "CB_TMA_TSTORE"])
+def test_fused_tma_store_modes_bitwise(cuda, mode, monkeypatch):
+    """K6's opt-in TMA-store epilogues (per-warp 32 x 32 boxes; 128-pixel boxes) store the
+    same values as the default per-lane stores: tiles inside and across images, bias, a
+    partial channel chunk."""
+    from paper_2407_10730_b200.algos import conv_fused
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    for d in (cfg("cfg4", batch=4),
+              ConvDescriptor(batch=3, in_channels=64, in_h=15, in_w=12, out_channels=200, k_h=3, k_w=3,
+                             pad_h=1, pad_w=1, has_bias=True)):
+        inp, (x, w, b) = _inputs(d)
+        y0 = conv_fused(inp, variant="tc3xbf16")
+        monkeypatch.setenv(mode, "1")
+        y1 = conv_fused(inp, variant="tc3xbf16")
+        monkeypatch.delenv(mode)
+        assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32)), d
