@@ -30,11 +30,14 @@
 namespace cb {
 
 constexpr int TS_BM = 128;
-constexpr int TS_PROD_WARPS = 12;  // three per TMEM lane quadrant
-constexpr int TS_EPI_WARP0 = 12;
-constexpr int TS_TMA_WARP = 16;
-constexpr int TS_MMA_WARP = 17;
-constexpr int TS_THREADS = 18 * 32;
+#ifndef CB_TS_KPARTS
+#define CB_TS_KPARTS 3
+#endif
+constexpr int TS_PROD_WARPS = 4 * CB_TS_KPARTS;  // CB_TS_KPARTS per TMEM lane quadrant
+constexpr int TS_EPI_WARP0 = TS_PROD_WARPS;
+constexpr int TS_TMA_WARP = TS_PROD_WARPS + 4;
+constexpr int TS_MMA_WARP = TS_PROD_WARPS + 5;
+constexpr int TS_THREADS = (TS_PROD_WARPS + 6) * 32;
 constexpr int TS_TMEM_COLS = 512;
 
 struct TsParams {
@@ -229,29 +232,31 @@ __device__ __forceinline__ void build_pairs(uint32_t xs_pair, uint32_t cstride, 
 template <int C, int R, int S>
 __device__ __forceinline__ void build_pairs_part(int kpart, uint32_t xs_pair, uint32_t cstride,
                                                  uint32_t rstride, uint32_t a_hi, uint32_t a_lo) {
-    constexpr int G = (C * R * (S + 1) + 7) / 8;
-    constexpr int G1 = (G + 2) / 3, G2 = G1 + (G - G1 + 1) / 2;
+    constexpr int G = (C * R * (S + 1) + 7) / 8, P = CB_TS_KPARTS;
     if (kpart == 0)
-        build_pairs<C, R, S, 0, G1>(xs_pair, cstride, rstride, a_hi, a_lo);
+        build_pairs<C, R, S, 0, G * 1 / P>(xs_pair, cstride, rstride, a_hi, a_lo);
     else if (kpart == 1)
-        build_pairs<C, R, S, G1, G2>(xs_pair, cstride, rstride, a_hi, a_lo);
-    else
-        build_pairs<C, R, S, G2, G>(xs_pair, cstride, rstride, a_hi, a_lo);
+        build_pairs<C, R, S, G * 1 / P, G * 2 / P>(xs_pair, cstride, rstride, a_hi, a_lo);
+    else if (kpart == 2)
+        build_pairs<C, R, S, G * 2 / P, G * 3 / P>(xs_pair, cstride, rstride, a_hi, a_lo);
+    else if (P > 3)
+        build_pairs<C, R, S, G * 3 / P, G>(xs_pair, cstride, rstride, a_hi, a_lo);
 }
 
-// the three producer warps of a lane quadrant take contiguous thirds of the 8-element groups
+// the producer warps of a lane quadrant take contiguous shares of the 8-element groups
 template <int C, int R, int S>
 __device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_t cstride,
                                                  uint32_t rstride, uint32_t a_hi, uint32_t a_lo,
                                                  bool swap) {
-    constexpr int G = (C * R * S + 7) / 8;
-    constexpr int G1 = (G + 2) / 3, G2 = G1 + (G - G1 + 1) / 2;
+    constexpr int G = (C * R * S + 7) / 8, P = CB_TS_KPARTS;
     if (kpart == 0)
-        build_fixed<C, R, S, 0, G1>(xs, cstride, rstride, a_hi, a_lo, swap);
+        build_fixed<C, R, S, 0, G * 1 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
     else if (kpart == 1)
-        build_fixed<C, R, S, G1, G2>(xs, cstride, rstride, a_hi, a_lo, swap);
-    else
-        build_fixed<C, R, S, G2, G>(xs, cstride, rstride, a_hi, a_lo, swap);
+        build_fixed<C, R, S, G * 1 / P, G * 2 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
+    else if (kpart == 2)
+        build_fixed<C, R, S, G * 2 / P, G * 3 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
+    else if (P > 3)
+        build_fixed<C, R, S, G * 3 / P, G>(xs, cstride, rstride, a_hi, a_lo, swap);
 }
 
 // compile-time reduction layouts (TsParams::fixed): 0 = generic offset-table producer
