@@ -534,7 +534,7 @@ def e2e_dropin(d, variant, x_h, w_h, calls: int = 10):
                                                    "value": algos.flop_count(d) / el / 1e9}
     assert y.shape == (d.batch, d.out_channels) + algos.output_shape(d)
     return {"unit": UNIT, "api": "algos.conv_fused(ConvInputs(numpy x, w)) -> numpy y (host clock, "
-                                 "synchronous; pageable copies)",
+                                 "synchronous; numpy copies through pinned staging buffers)",
             "h2d_bytes_per_call_uncached": int(x_h.nbytes + w_h.nbytes),
             "d2h_bytes_per_call": int(d.batch * d.out_channels * 4 *
                                       algos.output_shape(d)[0] * algos.output_shape(d)[1]), **out}
