@@ -113,3 +113,25 @@ def test_charts_from_report_csvs(tmp_path):
     assert (tmp_path / "s2.svg").read_bytes() == (tmp_path / "s.svg").read_bytes()
     (tmp_path / "bad.csv").write_text("key,flops\n")
     assert charts.main(["speedup", "--in", str(tmp_path / "bad.csv"), "--out", str(tmp_path / "x.svg")]) == 1
+
+
+def test_sweep_gpus_flag_dry_run(tmp_path):
+    """`tools/sweep.py --gpus 2 --dry-run` starts 2 ranks through the shared launcher (gloo):
+    the LPT partition covers every op exactly once across ranks, rank 0 gathers and writes
+    the reference-schema results CSVs and a summary for the whole job."""
+    import csv
+    import json
+    import subprocess
+    import sys
+    out = tmp_path / "sw"
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "sweep.py"), "--gpus", "2", "--dry-run",
+                        "--ops", "120", "--modes", "fused,main", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    summary = json.loads((out / "summary.json").read_text())
+    assert summary["world"] == 2 and summary["ops_run"] == 120
+    for m in ("fused", "main"):
+        rows = list(csv.reader(open(out / f"results_{m}.csv")))[1:]
+        assert len(rows) == 120 and all(row[2] == "ok" for row in rows)
+        busy = summary["modes"][m]["per_rank_busy_s"]
+        assert len(busy) == 2 and min(busy) > 0

@@ -89,7 +89,7 @@ def parser() -> argparse.ArgumentParser:
     ap.add_argument("--modes", default="fused,baseline,main")
     ap.add_argument("--warmups", type=int, default=3)
     ap.add_argument("--runs", type=int, default=10)
-    ap.add_argument("--variant", default=None, help="stepwise variant (default tc3xtf32)")
+    ap.add_argument("--variant", default=None, help=f"stepwise variant (default {algos.DEFAULT_VARIANT})")
     ap.add_argument("--fused-variant", default=algos.FUSED_AUTO)
     ap.add_argument("--device-inputs", action="store_true")
     ap.add_argument("--graph", action="store_true",
@@ -99,6 +99,9 @@ def parser() -> argparse.ArgumentParser:
     ap.add_argument("--out", default="sweep_out")
     ap.add_argument("--verbose", action="store_true", help="print every op key before it runs")
     ap.add_argument("--limit", type=int, default=0, help="diagnostics: run at most N ops per rank")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="the multi-rank plumbing on CPU (gloo): LPT partition, per-rank rows with "
+                         "the predicted time standing in for a measurement, gather, rank-0 outputs")
     return ap
 
 
@@ -130,7 +133,8 @@ def run(args, checker=None, ranks=None) -> int:
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    torch.cuda.set_device(local)
+    if not args.dry_run:
+        torch.cuda.set_device(local)
     if checker is not None and args.device_inputs:
         raise SystemExit("a parity check needs make_inputs host data (drop --device-inputs)")
 
@@ -153,6 +157,24 @@ def run(args, checker=None, ranks=None) -> int:
     busy = {m: 0.0 for m in modes}
     t0 = time.time()
     n = 0
+    while args.dry_run and n < len(mine):  # no GPU: predicted times stand in for measurements
+        from paper_2407_10730_b200.timing import _report, aggregate
+        i = mine[n]
+        d = descs[i]
+        for m in modes:
+            rf = roofline.conv_roofline(d, algos.resolve_variant(d, cfgs[m].variant), peaks)
+            el = [0] * len(Phase)
+            calls = [0] * len(Phase)
+            el[Phase.IN_MICROKERNEL] = int(predicted_s(d, peaks) * 1e9)
+            calls[Phase.IN_MICROKERNEL] = 1
+            o = harness.RunOutcome(key=key_of(d), mode=m, runs=1, warmups=0, status="ok",
+                                   stats=aggregate([_report(el, calls)]), detail="dry run")
+            t_op = o.stats.operation_ns_mean * 1e-9
+            busy[m] += t_op
+            local_rows[m].append({"index": i, "record": report.outcome_record(o), "status": o.status,
+                                  "flops": rf["flops"], "t_s": t_op, "t_min_s": t_op,
+                                  "roofline_s": rf["t_roofline_s"], "pack_share": None, "detail": o.detail})
+        n += 1
     while n < len(mine):
         d = descs[mine[n]]
         group = [mine[n]]
@@ -189,7 +211,8 @@ def run(args, checker=None, ranks=None) -> int:
         if rank == 0 and (n // 50) != ((n - len(group)) // 50):
             extra = checker.progress() if checker is not None else ""
             print(f"[rank0] {n}/{len(mine)} ops, {time.time() - t0:.0f} s {extra}", flush=True)
-    torch.cuda.empty_cache()
+    if not args.dry_run:
+        torch.cuda.empty_cache()
     parity = checker.finish() if checker is not None else None
 
     gathered = [None] * world
@@ -216,7 +239,8 @@ def write_outputs(args, descs, idx, modes, gathered, model_ops, peaks, world, wa
                "inputs": "device (torch.rand, not make_inputs bits)" if args.device_inputs
                else "make_inputs (bit-identical to the reference), uploaded once per op key",
                "warmups": args.warmups, "runs": args.runs, "peaks": peaks,
-               "timing": "CUDA-graph replay per op (device phases, no host launch gaps)"
+               "timing": "dry run: predicted times, no GPU" if args.dry_run else
+               "CUDA-graph replay per op (device phases, no host launch gaps)"
                if args.graph else "eager calls (device phases include launch latency)",
                "modes": {}}
     parity = {}
