@@ -61,7 +61,8 @@ struct TmaParams {
     int64_t total_tiles;  // n_tiles * m_tiles * G * splits
     int add_mode;         // 0: store acc + bias, 1: fp32 reduction into out
     int tma_store;        // 1: epilogue stages 32-channel chunks in smem, TMA-stores y (tm_y);
-                          // 2: per epilogue warp, 32 pixels x 32 channels per TMA store
+                          // 2: per epilogue warp, 32 pixels x 32 channels per TMA store;
+                          // 3: mode 2 for the cluster's last item only
     int bulk_parts;       // 1: tail parts write their partial chunks with 1-D bulk copies
     int out_al16;         // 1: y is 16-byte aligned (the tail fixup's float4 stores need it)
     // Accumulator promotion (see promote_k): an item's K blocks run as ranges of at most
@@ -657,8 +658,10 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
             // per-warp TMA stores: this warp's 32 pixel rows all valid and in one image
             const int64_t mw = m0t + quad * 32;
             const int64_t nw = mw / g.PQ;
-            const bool warp_tstore = p.tma_store == 2 && !promoted && !(p.debug & 2) &&
-                                     mw + 31 < g.npix && (mw + 31) / g.PQ == nw;
+            // (mode 3: only on the cluster's last item, when the TMA unit has no operand loads
+            // left to serve)
+            const bool warp_tstore = (p.tma_store == 2 || (p.tma_store == 3 && t + ncl >= p.total_items)) &&
+                                     !promoted && !(p.debug & 2) && mw + 31 < g.npix && (mw + 31) / g.PQ == nw;
 #pragma unroll 1
             for (int ci = 0; ci < nchunk; ++ci) {
                 const int c0 = ci * 32;
@@ -678,8 +681,10 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                     // [32 ch][32 px] (+bias) of this warp staged in its own 4 KB and stored by
                     // the TMA engine: no epilogue barrier, and the engine keeps the NCHW
                     // writes in flight (K8 / K7 measured 2x faster than per-lane stores)
-                    float* buf = ostage + quad * (32 * 32);
-                    if (lane == 0) ptx::bulk_wait_read<0>();  // this warp's last store left buf
+                    // two 4 KB buffers per warp (the 32 KB ostage): the store of chunk ci - 1
+                    // may still be reading the other one
+                    float* buf = ostage + (quad * 2 + (ci & 1)) * (32 * 32);
+                    if (lane == 0) ptx::bulk_wait_read<1>();  // the store 2 chunks ago left buf
                     __syncwarp();
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
@@ -1083,7 +1088,7 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
         auto fn = tiled_encode_fn();
         cuuint64_t dims[3] = {(cuuint64_t)prm.g.PQ, (cuuint64_t)prm.g.K, (cuuint64_t)prm.g.N};
         cuuint64_t strides[2] = {(cuuint64_t)prm.g.PQ * 4, (cuuint64_t)prm.g.K * prm.g.PQ * 4};
-        cuuint32_t box[3] = {(cuuint32_t)(prm.tma_store == 2 ? 32 : TMA_BM), 32, 1};
+        cuuint32_t box[3] = {(cuuint32_t)(prm.tma_store >= 2 ? 32 : TMA_BM), 32, 1};
         cuuint32_t es[3] = {1, 1, 1};
         CUresult r = fn(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, prm.out, dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1217,7 +1222,8 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     // loads) -- unlike K7 and K8, whose epilogues are exposed.  Both TMA modes are opt-in.
     const bool ymap_ok = (g.PQ % 4 == 0) && (g.G == 1 || g.kpg % 32 == 0) &&
                          (reinterpret_cast<uintptr_t>(y) & 15) == 0;
-    prm.tma_store = !ymap_ok ? 0 : std::getenv("CB_TMA_TSTORE") ? 1 : std::getenv("CB_TMA_WSTORE") ? 2 : 0;
+    prm.tma_store = !ymap_ok ? 0 : std::getenv("CB_TMA_TSTORE") ? 1 : std::getenv("CB_TMA_WSTORE") ? 2
+                    : std::getenv("CB_TMA_LASTW") ? 3 : 0;
     prm.bulk_parts = std::getenv("CB_TMA_BULK_PARTS") ? 1 : 0;
     prm.out_al16 = (reinterpret_cast<uintptr_t>(y) & 15) == 0 ? 1 : 0;
     prm.range_kb = std::max(1, promote_k(bf16) / (128 / L.eb));
