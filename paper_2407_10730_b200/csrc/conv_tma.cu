@@ -60,9 +60,7 @@ struct TmaParams {
     int kb_per_split;
     int64_t total_tiles;  // n_tiles * m_tiles * G * splits
     int add_mode;         // 0: store acc + bias, 1: fp32 reduction into out
-    int tma_store;        // 1: epilogue stages 32-channel chunks in smem, TMA-stores y (tm_y);
-                          // 2: per epilogue warp, 32 pixels x 32 channels per TMA store;
-                          // 3: mode 2 for the cluster's last item only
+    int tma_store;        // 1: epilogue stages 32-channel chunks in smem, TMA-stores y (tm_y)
     int bulk_parts;       // 1: tail parts write their partial chunks with 1-D bulk copies
     int out_al16;         // 1: y is 16-byte aligned (the tail fixup's float4 stores need it)
     // Accumulator promotion (see promote_k): an item's K blocks run as ranges of at most
@@ -610,7 +608,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                         // STG.128 instead of a 128-byte one per STG.32
                         float* buf = ostage + (ochunk & 1) * (32 * TMA_BM);
                         ++ochunk;
-                        if (lane == 0) ptx::bulk_wait_read<0>();  // no TMA store (any warp's) reads buf
+                        if (threadIdx.x == 0) ptx::bulk_wait_read<0>();  // no TMA store reads buf
                         epi_barrier();
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -653,15 +651,8 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
             // pixel coordinate); tiles across an image boundary store directly
             const int64_t m0t = it.mt * (TMA_BM * CG) + rank * TMA_BM;
             const int64_t n0t = m0t / g.PQ;
-            const bool tile_tstore = p.tma_store == 1 && !promoted && m0t < g.npix &&
+            const bool tile_tstore = p.tma_store && !promoted && m0t < g.npix &&
                                      (min(m0t + TMA_BM, g.npix) - 1) / g.PQ == n0t;
-            // per-warp TMA stores: this warp's 32 pixel rows all valid and in one image
-            const int64_t mw = m0t + quad * 32;
-            const int64_t nw = mw / g.PQ;
-            // (mode 3: only on the cluster's last item, when the TMA unit has no operand loads
-            // left to serve)
-            const bool warp_tstore = (p.tma_store == 2 || (p.tma_store == 3 && t + ncl >= p.total_items)) &&
-                                     !promoted && !(p.debug & 2) && mw + 31 < g.npix && (mw + 31) / g.PQ == nw;
 #pragma unroll 1
             for (int ci = 0; ci < nchunk; ++ci) {
                 const int c0 = ci * 32;
@@ -677,26 +668,7 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                     else
                         ptx::mbar_arrive(&tempty[acc]);
                 }
-                if (warp_tstore && nvalid == 32) {
-                    // [32 ch][32 px] (+bias) of this warp staged in its own 4 KB and stored by
-                    // the TMA engine: no epilogue barrier, and the engine keeps the NCHW
-                    // writes in flight (K8 / K7 measured 2x faster than per-lane stores)
-                    // two 4 KB buffers per warp (the 32 KB ostage): the store of chunk ci - 1
-                    // may still be reading the other one
-                    float* buf = ostage + (quad * 2 + (ci & 1)) * (32 * 32);
-                    if (lane == 0) ptx::bulk_wait_read<1>();  // the store 2 chunks ago left buf
-                    __syncwarp();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        buf[i * 32 + lane] = __uint_as_float(r[i]) + (bias ? __ldg(bias + c0 + i) : 0.f);
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        ptx::tma_store_3d(&tm_y, buf, (int32_t)(mw - nw * g.PQ), gi * g.kpg + f_tile0 + c0,
-                                          (int32_t)nw);
-                        ptx::bulk_commit();
-                    }
-                } else if (tile_tstore && !(p.debug & 2)) {
+                if (tile_tstore && !(p.debug & 2)) {
                     // stage [32 ch][128 px] (+bias) and TMA-store it (the tensor map clips
                     // the image's last tile)
                     float* buf = ostage + (ochunk & 1) * (32 * TMA_BM);
@@ -740,8 +712,10 @@ conv_tma_kernel(const __grid_constant__ TmaParams p, const __grid_constant__ CUt
                 dst += (int64_t)32 * g.PQ;
             }
         }
-        if (lane == 0) ptx::bulk_wait_all();  // smem sources must outlive the bulk stores
-        if (threadIdx.x == 0) trace_stamp(p, TRACE_SLOTS - 1);  // epilogue finished
+        if (threadIdx.x == 0) {
+            ptx::bulk_wait_all();  // smem sources must outlive the bulk stores
+            trace_stamp(p, TRACE_SLOTS - 1);  // epilogue finished
+        }
     }
 
     ptx::tc_fence_before();
@@ -1084,11 +1058,11 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     if ((rc = make_act_map(&mal, BF16, prm.g, prm.L, alo))) return rc;
     if ((rc = make_w_map(&mwh, BF16, whi, prm.g.K, prm.L.kw_pad, Cfg::B_ROWS))) return rc;
     if ((rc = make_w_map(&mwl, BF16, wlo, prm.g.K, prm.L.kw_pad, Cfg::B_ROWS))) return rc;
-    if (prm.tma_store) {  // y as {PQ, K, N}, boxes of 128 (mode 1) or 32 (mode 2) pixels x 32 channels
+    if (prm.tma_store) {  // y as {PQ, K, N}, boxes of 128 pixels x 32 channels
         auto fn = tiled_encode_fn();
         cuuint64_t dims[3] = {(cuuint64_t)prm.g.PQ, (cuuint64_t)prm.g.K, (cuuint64_t)prm.g.N};
         cuuint64_t strides[2] = {(cuuint64_t)prm.g.PQ * 4, (cuuint64_t)prm.g.K * prm.g.PQ * 4};
-        cuuint32_t box[3] = {(cuuint32_t)(prm.tma_store >= 2 ? 32 : TMA_BM), 32, 1};
+        cuuint32_t box[3] = {(cuuint32_t)TMA_BM, 32, 1};
         cuuint32_t es[3] = {1, 1, 1};
         CUresult r = fn(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, prm.out, dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1216,14 +1190,8 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     // (CB_TMA_BULK_PARTS): measured equal or slower than the direct stores on cfg4 and on
     // output-heavy sweep ops (two epilogue barriers per chunk; tiles crossing images fall
     // back to direct stores anyway), so both are off by default.
-    // Per-warp 32 x 32 TMA stores (mode 2, CB_TMA_WSTORE) measured slower here than the
-    // per-lane stores: cfg4 K6 58.4 -> 61.0 us, step 68.8 -> 71.1 us (the epilogue overlaps
-    // the next tile's MMAs, and its stores then queue in the TMA unit behind the im2col
-    // loads) -- unlike K7 and K8, whose epilogues are exposed.  Both TMA modes are opt-in.
-    const bool ymap_ok = (g.PQ % 4 == 0) && (g.G == 1 || g.kpg % 32 == 0) &&
-                         (reinterpret_cast<uintptr_t>(y) & 15) == 0;
-    prm.tma_store = !ymap_ok ? 0 : std::getenv("CB_TMA_TSTORE") ? 1 : std::getenv("CB_TMA_WSTORE") ? 2
-                    : std::getenv("CB_TMA_LASTW") ? 3 : 0;
+    prm.tma_store = (g.PQ % 4 == 0) && (g.G == 1 || g.kpg % 32 == 0) &&
+                    (reinterpret_cast<uintptr_t>(y) & 15) == 0 && std::getenv("CB_TMA_TSTORE");
     prm.bulk_parts = std::getenv("CB_TMA_BULK_PARTS") ? 1 : 0;
     prm.out_al16 = (reinterpret_cast<uintptr_t>(y) & 15) == 0 ? 1 : 0;
     prm.range_kb = std::max(1, promote_k(bf16) / (128 / L.eb));

@@ -493,9 +493,9 @@ def test_stepwise_tail_splits(cuda, spec, monkeypatch):
 
 
 
-@pytest.mark.parametrize("mode", ["CB_TMA_WSTORE", "CB_TMA_TSTORE"])
+@pytest.mark.parametrize("mode", ["CB_TMA_TSTORE"])
 def test_fused_tma_store_modes_bitwise(cuda, mode, monkeypatch):
-    """K6's opt-in TMA-store epilogues (per-warp 32 x 32 boxes; 128-pixel boxes) store the
+    """K6's opt-in TMA-store epilogue (128-pixel boxes for tiles inside one image) stores the
     same values as the default per-lane stores: tiles inside and across images, bias, a
     partial channel chunk."""
     from paper_2407_10730_b200.algos import conv_fused
