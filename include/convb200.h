@@ -50,10 +50,12 @@ typedef struct cb_conv_desc {
 /* SConv slice plan: a slice is one band of `band_rows` output rows over the full
  * output width of one image (the GPU counterpart of _TilePlan, algos.py:247-262).
  * Slices tile the (n, oy, ox) pixel range contiguously.  The SConv calls take a slice
- * range [first_slice, first_slice + count) = pixels [jb, je) and a slice buffer that
- * starts at pixel jb: the slice holding pixels [j0, j0+np) lives at
- * slices + C*R*S*(j0 - jb), laid out (k, pixel); the accumulator buffer likewise at
- * acc + K*(j0 - jb), laid out (f, pixel).  Ranges are processed as L2-resident chunks. */
+ * range [first_slice, first_slice + count) = pixels [jb, je), J = je - jb.  Its slice
+ * buffer is the (C*R*S) x J matrix of the range's im2col columns, laid out (k, pixel) with
+ * row stride J: the slice holding pixels [j0, j0+np) is the column block [j0-jb, j0-jb+np)
+ * (panels of consecutive slices are adjacent, so the GEMM's 128-pixel tiles run across
+ * slice boundaries).  The accumulators are likewise a K x J matrix, (f, pixel).  Ranges are
+ * processed as chunks sized for the grid. */
 typedef struct cb_slice_plan {
     int32_t band_rows;   /* output rows per slice (last band of an image may be shorter) */
     int32_t num_slices;  /* batch * ceil(out_h / band_rows)                              */

@@ -104,9 +104,10 @@ int make_geom(const cb_conv_desc* d, Geom* g) {
 }
 
 int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
-                       int first_slice, int count, int64_t j_begin, cudaStream_t st);
-int launch_im2col(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
-                  int64_t j_begin, int64_t j_count, cudaStream_t st);
+                       int first_slice, int count, int64_t j_begin, int64_t j_count,
+                       cudaStream_t st);
+int launch_im2col(const Geom& g, const float* x, float* out, int64_t j_begin, int64_t j_count,
+                  cudaStream_t st);
 int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float* w, void* hi,
                         void* lo, cudaStream_t st);
 int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count,
@@ -294,9 +295,9 @@ int cb_im2col_f32(const cb_conv_desc* d, const float* x, float* cols, void* stre
     if (rc) return rc;
     if (!x || !cols) return fail(CB_ERR_INVALID, "null buffer");
     // smem-staged band kernel; the per-element kernel covers windows too wide for smem
-    rc = launch_im2col_band(g, x, cols, false, 0, 0, 0, 0, (cudaStream_t)stream);
+    rc = launch_im2col_band(g, x, cols, false, 0, 0, 0, 0, g.npix, (cudaStream_t)stream);
     if (rc != CB_ERR_UNSUPPORTED) return rc;
-    return launch_im2col(g, x, cols, false, 1, 0, g.npix, (cudaStream_t)stream);
+    return launch_im2col(g, x, cols, 0, g.npix, (cudaStream_t)stream);
 }
 
 int cb_sconv_plan(const cb_conv_desc* d, int32_t max_slice_pixels, cb_slice_plan* plan) {
@@ -332,10 +333,10 @@ int cb_sconv_pack_f32(const cb_conv_desc* d, const cb_slice_plan* plan, int32_t 
     int64_t jb, jc;
     if ((rc = slice_range(g, plan, first_slice, count, &jb, &jc))) return rc;
     if (count == 0) return CB_OK;
-    rc = launch_im2col_band(g, x, slices, true, plan->band_rows, first_slice, count, jb,
+    rc = launch_im2col_band(g, x, slices, true, plan->band_rows, first_slice, count, jb, jc,
                             (cudaStream_t)stream);
     if (rc != CB_ERR_UNSUPPORTED) return rc;
-    return launch_im2col(g, x, slices, true, plan->band_rows, jb, jc, (cudaStream_t)stream);
+    return launch_im2col(g, x, slices, jb, jc, (cudaStream_t)stream);
 }
 
 int cb_plan_tiles(int variant, const cb_conv_desc* d, int64_t pixels, cb_tile_plan* plan) {
@@ -426,11 +427,18 @@ int cb_sconv_gemm(int variant, const cb_conv_desc* d, const cb_slice_plan* plan,
     if (rc) return rc;
     if ((rc = sconv_supported(g)) || (rc = check_plan(g, plan))) return rc;
     if (!slices || !acc) return fail(CB_ERR_INVALID, "null buffer");
+    int64_t jb, jc;
+    if ((rc = slice_range(g, plan, first_slice, count, &jb, &jc))) return rc;
+    // the chunk's slice buffer is the (kdim x jc) im2col matrix of its pixels and the
+    // accumulators a (K x jc) matrix: a plain GEMM over launch-local pixels, whose tiles
+    // run across slice boundaries
     PixMap pm{};
-    if ((rc = slice_range(g, plan, first_slice, count, &pm.j_begin, &pm.j_count))) return rc;
-    pm.src_mode = SRC_SLICES;
-    pm.dst_mode = DST_SLICES;
-    pm.band_rows = plan->band_rows;
+    pm.src_mode = SRC_MATRIX;
+    pm.dst_mode = DST_MATRIX;
+    pm.src_ld = jc;
+    pm.dst_ld = jc;
+    pm.j_begin = 0;
+    pm.j_count = jc;
     return run_variant(variant, g, pm, slices, w_hi, w_lo, w_f32, nullptr, acc, 0,
                        /*zero_kind=contiguous memset*/ 2, (cudaStream_t)stream);
 }

@@ -59,48 +59,30 @@ int promote_k(bool bf16);  // defaults: 2048 (tf32 MMAs, K = 8 each), 4096 (bf16
 // and "reduction" k in [0, kdim).  Source (activation-side) operands are either
 // gathered from NCHW (implicit im2col) or linear in k per pixel:
 //     addr(j, k) = base(j) + k * kstride(j)
-// which covers the im2col matrix (base=j, kstride=ld) and the SConv slice buffer
-// (base = kdim*j0 + (j-j0), kstride = slice pixels).  Outputs are always linear:
+// which covers the im2col matrix (base=j, kstride=ld).  The SConv slice buffer of a
+// chunk is such a matrix too: the im2col columns of the chunk's pixels [jb, jb+J),
+// (k, pixel) with row stride J, so the SConv GEMM runs in matrix mode with launch-local
+// pixels.  Outputs are always linear:
 //     out(j, f) = obase(j) + f * okstride(j)
-// covering NCHW (obase = n*K*PQ + p, okstride = PQ), a plain row-major matrix and the
-// per-slice accumulator buffer.
+// covering NCHW (obase = n*K*PQ + p, okstride = PQ) and a row-major matrix (the SConv
+// accumulators of a chunk: (f, pixel), row stride J).
 // ------------------------------------------------------------------------------------
-enum SrcMode : int { SRC_CONV = 0, SRC_MATRIX = 1, SRC_SLICES = 2 };
-enum DstMode : int { DST_NCHW = 0, DST_MATRIX = 1, DST_SLICES = 2 };
+enum SrcMode : int { SRC_CONV = 0, SRC_MATRIX = 1 };
+enum DstMode : int { DST_NCHW = 0, DST_MATRIX = 1 };
 
 struct PixMap {
     int src_mode, dst_mode;
     int64_t src_ld;      // SRC_MATRIX row stride (group g starts at row g*kdim)
     int64_t dst_ld;      // DST_MATRIX row stride
-    int band_rows;       // SLICES: output rows per slice
-    int64_t j_begin;     // first pixel of this launch; slice buffers start at this pixel
+    int64_t j_begin;     // first pixel of this launch
     int64_t j_count;     // pixels processed by this launch
 };
 
-__device__ __forceinline__ void slice_of(const Geom& g, int band_rows, int64_t j, int64_t& j0,
-                                         int& np) {
-    int64_t n = j / g.PQ;
-    int p = (int)(j - n * g.PQ);
-    int oy = p / g.Q;
-    int y0 = (oy / band_rows) * band_rows;
-    int rows = min(band_rows, g.P - y0);
-    np = rows * g.Q;
-    j0 = n * g.PQ + (int64_t)y0 * g.Q;
-}
-
-// Linear source address components for pixel j (SRC_MATRIX / SRC_SLICES).
+// Linear source address components for pixel j (SRC_MATRIX).
 __device__ __forceinline__ void src_linear(const Geom& g, const PixMap& pm, int64_t j,
                                            int64_t& base, int64_t& kstride) {
-    if (pm.src_mode == SRC_MATRIX) {
-        base = j;
-        kstride = pm.src_ld;
-    } else {
-        int64_t j0;
-        int np;
-        slice_of(g, pm.band_rows, j, j0, np);
-        base = (int64_t)g.kdim * (j0 - pm.j_begin) + (j - j0);
-        kstride = np;
-    }
+    base = j;
+    kstride = pm.src_ld;
 }
 
 // Output address components for pixel j.
@@ -111,15 +93,9 @@ __device__ __forceinline__ void dst_linear(const Geom& g, const PixMap& pm, int6
         int64_t p = j - n * g.PQ;
         base = n * (int64_t)g.K * g.PQ + p;
         okstride = g.PQ;
-    } else if (pm.dst_mode == DST_MATRIX) {
+    } else {
         base = j;
         okstride = pm.dst_ld;
-    } else {
-        int64_t j0;
-        int np;
-        slice_of(g, pm.band_rows, j, j0, np);
-        base = (int64_t)g.K * (j0 - pm.j_begin) + (j - j0);
-        okstride = np;
     }
 }
 

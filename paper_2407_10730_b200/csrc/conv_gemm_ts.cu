@@ -53,8 +53,6 @@ struct G8Params {
     int ring;         // A chunks in the TMEM ring
     int bstages;      // smem weight stages
     int tma_a;        // 1: A chunks arrive by TMA into smem, 0: per-thread loads
-    int tps;          // > 0: SConv slices, tiles never cross a slice: tps tiles per slice of np px
-    int np;
     // Tail N-split: items [0, full_items) are whole tiles; each of the remaining tiles (the
     // ragged last wave) is cut into tail_split channel ranges (multiples of 16 columns), one
     // item each, so the last wave keeps every SM busy.  A is rebuilt per range.
@@ -77,10 +75,10 @@ struct G8Params {
     unsigned long long* trace;  // diagnostics (CB_K8_TRACE): per-CTA globaltimer stamps
     int astages;                // A chunk stages in smem (TMA sources)
     int debug;                  // diagnostics (CB_K8_DEBUG): 1 no weight TMA, 2 no A TMA, 4 no MMA, 8 no A build, 16 no epilogue stores, 32 no bias
-    // TMA-store epilogue (tma_y = 1: NCHW y as {PQ, K, N}; 2: slice accumulators as {np, K,
-    // slices}): an epilogue warp stages its 32 rows x 32 channels in smem and one lane
-    // stores them with the TMA engine; warps whose rows cross an image or hold invalid rows,
-    // partial channel chunks and read-add-write ranges use per-lane stores
+    // TMA-store epilogue (tma_y = 1: NCHW y as {PQ, K, N}; 2: a row-major output matrix as
+    // {ld, rows, 1}, e.g. the SConv accumulators): an epilogue warp stages its 32 rows x 32
+    // channels in smem and one lane stores them with the TMA engine; warps whose rows cross
+    // an image or hold invalid rows and partial channel chunks use per-lane stores
     int tma_y;
 };
 
@@ -195,14 +193,8 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
     const int nch = p.nchunks;
     if (threadIdx.x == 0) g8_stamp(p, 31);
 
-    // pixel tile mt, row m -> launch-local pixel jl (slice-aligned tiles for slice sources)
+    // pixel tile mt, row m -> launch-local pixel jl
     auto pix_of = [&](int64_t mt, int m, int64_t& jl) -> bool {
-        if (p.tps) {
-            const int64_t sl = mt / p.tps;
-            const int off = (int)(mt - sl * p.tps) * G8_BM + m;
-            jl = sl * p.np + off;
-            return off < p.np;
-        }
         jl = mt * G8_BM + m;
         return jl < p.pm.j_count;
     };
@@ -388,8 +380,8 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 const int nvalid = min(32, ncol - c0);
                 const int fb = gi * g.kpg + f_tile0 + c0;
                 // TMA store (or TMA add for later ranges / K parts / add_mode) of this warp's
-                // 32 x 32 block: every row valid and in one image (NCHW) / slice, a whole
-                // channel chunk
+                // 32 x 32 block: every row valid and in one image (NCHW), a whole channel
+                // chunk
                 bool tma_ok = p.tma_y && nvalid == 32 && !(p.debug & 16) && __all_sync(0xffffffffu, jvalid);
                 int32_t yc0 = 0, yc2 = 0;
                 if (tma_ok) {
@@ -398,13 +390,11 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                         const int64_t n = ja / g.PQ;
                         yc0 = (int32_t)(ja - n * g.PQ);
                         yc2 = (int32_t)n;
-                    } else {  // slice-aligned tile: slice mt / tps, pixel offset within it
-                        const int64_t sl = mt / p.tps;
-                        yc0 = (int32_t)((mt - sl * p.tps) * G8_BM + m);
-                        yc2 = (int32_t)sl;
+                    } else {  // output matrix: column ja
+                        yc0 = (int32_t)ja;
                     }
                     const int32_t y2_0 = __shfl_sync(0xffffffffu, yc2, 0);
-                    tma_ok = __all_sync(0xffffffffu, y2_0 == yc2);  // one image / slice
+                    tma_ok = __all_sync(0xffffffffu, y2_0 == yc2);  // one image
                     yc0 = __shfl_sync(0xffffffffu, yc0, 0);
                     yc2 = y2_0;
                 }
@@ -477,8 +467,6 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                 decode(t, nt, mt, gi);
                 const int x0 = (int)(p.pm.j_begin + mt * G8_BM);
                 const int row0 = gi * g.kdim;
-                const int64_t sl = p.tps ? mt / p.tps : 0;
-                const int xs = p.tps ? (int)(mt - sl * p.tps) * G8_BM : 0;
                 for (int kc = k_lo; kc < k_hi; ++kc, as = as + 1 == p.astages ? 0 : as + 1,
                          asph ^= (as == 0 ? 1u : 0u)) {
                     const int64_t cg = cbase + (kc - k_lo);
@@ -488,11 +476,7 @@ gemm_ts_kernel(const __grid_constant__ G8Params p, const __grid_constant__ CUten
                         ptx::mbar_arrive(&as_full[as]);  // diagnostics: stale A chunk
                     } else if (leader) {
                         ptx::mbar_arrive_expect_tx(&as_full[as], G8_ASTAGE_BYTES);
-                        if (p.tps)  // slice buffer as {np, kdim, slices}
-                            ptx::tma_load_3d(astage + (size_t)as * (32 * G8_BM), &tm_a, &as_full[as], xs,
-                                             kc * G8_CK, (int32_t)sl);
-                        else
-                            ptx::tma_load_2d(astage + (size_t)as * (32 * G8_BM), &tm_a, &as_full[as], x0,
+                        ptx::tma_load_2d(astage + (size_t)as * (32 * G8_BM), &tm_a, &as_full[as], x0,
                                              row0 + kc * G8_CK);
                     }
                     __syncwarp();
@@ -662,18 +646,7 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
             return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string((int)r));
     }
     CUtensorMap ma{};
-    if (prm.tma_a && prm.tps) {  // slices [count][kdim][np], boxes of 128 pixels x 32 rows
-        cuuint64_t dims[3] = {(cuuint64_t)prm.np, (cuuint64_t)prm.g.kdim,
-                              (cuuint64_t)(prm.pm.j_count / prm.np)};
-        cuuint64_t strides[2] = {(cuuint64_t)prm.np * 4, (cuuint64_t)prm.g.kdim * prm.np * 4};
-        cuuint32_t box[3] = {(cuuint32_t)G8_BM, (cuuint32_t)G8_CK, 1};
-        cuuint32_t es[3] = {1, 1, 1};
-        CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(prm.src), dims,
-                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS)
-            return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled (slices) failed: " + std::to_string((int)r));
-    } else if (prm.tma_a) {  // the fp32 matrix [rows][ld], boxes of 128 pixels x 32 rows
+    if (prm.tma_a) {  // the fp32 matrix [rows][ld], boxes of 128 pixels x 32 rows
         cuuint64_t dims[2] = {(cuuint64_t)prm.pm.src_ld, (cuuint64_t)prm.g.G * prm.g.kdim};
         cuuint64_t strides[1] = {(cuuint64_t)prm.pm.src_ld * 4};
         cuuint32_t box[2] = {(cuuint32_t)G8_BM, (cuuint32_t)G8_CK};
@@ -711,10 +684,10 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
         }
     }
     CUtensorMap my{};
-    if (prm.tma_y) {  // NCHW y {PQ, K, N} or slice accumulators {np, K, slices}, 32 x 32 boxes
+    if (prm.tma_y) {  // NCHW y {PQ, K, N} or an output matrix {ld, K, 1}, 32 x 32 boxes
         const bool nchw = prm.tma_y == 1;
-        const cuuint64_t inner = nchw ? (cuuint64_t)prm.g.PQ : (cuuint64_t)prm.np;
-        const cuuint64_t outer = nchw ? (cuuint64_t)prm.g.N : (cuuint64_t)(prm.pm.j_count / prm.np);
+        const cuuint64_t inner = nchw ? (cuuint64_t)prm.g.PQ : (cuuint64_t)prm.pm.dst_ld;
+        const cuuint64_t outer = nchw ? (cuuint64_t)prm.g.N : 1;
         cuuint64_t dims[3] = {inner, (cuuint64_t)prm.g.K, outer};
         cuuint64_t strides[2] = {inner * 4, inner * prm.g.K * 4};
         cuuint32_t box[3] = {32, 32, 1};
@@ -752,14 +725,6 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
     int bn = g.kpg <= 64 ? 64 : g.kpg <= 128 ? 128 : 256;
     if (const char* e = std::getenv("CB_K8_BN")) bn = std::min(bn, std::max(64, std::atoi(e)));  // diagnostics
     prm.m_tiles = (pm.j_count + G8_BM - 1) / G8_BM;
-    const bool slice_tma = pm.src_mode == SRC_SLICES && pm.band_rows > 0 &&
-                           g.P % pm.band_rows == 0 && (pm.band_rows * g.Q) % 4 == 0 &&
-                           pm.j_count % (pm.band_rows * g.Q) == 0 &&
-                           (reinterpret_cast<uintptr_t>(src) & 15) == 0 && !std::getenv("CB_K8_NO_TMA_A");
-    if (slice_tma) {  // slice-aligned tiles
-        const int npx = pm.band_rows * g.Q;
-        prm.m_tiles = (pm.j_count / npx) * ((npx + G8_BM - 1) / G8_BM);
-    }
     // (narrower channel tiles for short grids measured slower: A is rebuilt per channel tile)
     prm.n_tiles = (g.kpg + bn - 1) / bn;
     prm.items = prm.m_tiles * prm.n_tiles * g.G;
@@ -798,21 +763,13 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
     prm.tma_a = pm.src_mode == SRC_MATRIX && (pm.src_ld % 4) == 0 &&
                 (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pm.j_begin + pm.j_count <= pm.src_ld &&
                 !std::getenv("CB_K8_NO_TMA_A");
-    // SConv slices: equal slices (P a multiple of the band) of a 16-byte multiple of pixels
-    // -> slice-aligned tiles, A chunks by a 3-D TMA over {np, kdim, slices}
-    const int np = pm.band_rows * g.Q;
-    if (slice_tma) {
-        prm.tma_a = 1;
-        prm.np = np;
-        prm.tps = (np + G8_BM - 1) / G8_BM;
-    }
-    // TMA-store epilogue: NCHW y (the Im2col-GEMM drop-in) or equal slice-aligned accumulators
-    // (SConv); 16-byte row strides and base
+    // TMA-store epilogue: NCHW y (the Im2col-GEMM drop-in) or an output matrix (the SConv
+    // accumulators, cb_gemm); 16-byte row strides and base
     prm.tma_y = 0;
     if (!std::getenv("CB_K8_NO_TMA_STORE") && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !add_mode) {
         if (pm.dst_mode == DST_NCHW && g.PQ % 4 == 0 && pm.j_begin == 0)
             prm.tma_y = 1;
-        else if (pm.dst_mode == DST_SLICES && prm.tps && prm.np % 4 == 0)
+        else if (pm.dst_mode == DST_MATRIX && pm.dst_ld % 4 == 0)
             prm.tma_y = 2;
     }
     switch (bn) {

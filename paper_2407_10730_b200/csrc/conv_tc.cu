@@ -5,7 +5,7 @@
 //   * conv_fused       (SRC_CONV):   the whole conv, activations gathered from NCHW
 //                                    (implicit im2col, no workspace)         -> K6
 //   * the im2col GEMM  (SRC_MATRIX): gemm(wmat, cols) of algos.py:142-182,203-208 -> K4
-//   * the SConv GEMM   (SRC_SLICES): wmat[f0:f1] @ pmat of algos.py:326-330      -> K4
+//   * the SConv GEMM   (SRC_MATRIX, a chunk's slices): wmat[f0:f1] @ pmat of algos.py:326-330 -> K4
 //
 // GEMM mapping (per group gi):
 //   M  = pixels j (128 per CTA tile, one TMEM lane each)
@@ -38,7 +38,7 @@ namespace cb {
 struct TcParams {
     Geom g;
     PixMap pm;
-    const float* src;   // x (SRC_CONV), cols / b matrix (SRC_MATRIX), slices (SRC_SLICES)
+    const float* src;   // x (SRC_CONV), cols / b matrix / SConv slices (SRC_MATRIX)
     const float* bias;  // (K,) or null; only added in store mode
     float* out;
     int num_kb;         // k blocks of BK over kdim

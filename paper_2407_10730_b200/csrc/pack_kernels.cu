@@ -25,10 +25,9 @@ namespace cb {
 constexpr int PACK_VEC = 4;
 constexpr int PACK_THREADS = 256;
 
-template <bool SLICED>
 __global__ void __launch_bounds__(PACK_THREADS)
-im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ out, int band_rows,
-              int64_t j_begin, int64_t j_count, int64_t col_blocks, bool vec_ok) {
+im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ out, int64_t j_begin,
+              int64_t j_count, int64_t col_blocks, bool vec_ok) {
     const int64_t bid = blockIdx.x;
     const int row = (int)(bid / col_blocks);
     const int64_t cblk = bid - (int64_t)row * col_blocks;
@@ -67,36 +66,14 @@ im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ out, int 
         }
     }
 
-    if (!SLICED) {
-        float* dst = out + (int64_t)row * j_count + jl;
-        if (vec_ok) {
-            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < PACK_VEC; ++i)
-                if (jl + i < j_count) dst[i] = v[i];
-        }
+    // (k, pixel) with row stride j_count: the im2col columns (K1) or a chunk's slices (K2)
+    float* dst = out + (int64_t)row * j_count + jl;
+    if (vec_ok) {
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
-        // slice buffer: the slice holding pixels [j0, j0+np) starts at
-        // out + kdim*(j0 - j_begin), laid out (k, pixel)
-        if (vec_ok) {
-            int64_t j0;
-            int np;
-            slice_of(g, band_rows, j, j0, np);
-            float* dst = out + (int64_t)g.kdim * (j0 - j_begin) + (int64_t)row * np + (j - j0);
-            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
 #pragma unroll
-            for (int i = 0; i < PACK_VEC; ++i) {
-                if (jl + i < j_count) {
-                    int64_t j0;
-                    int np;
-                    slice_of(g, band_rows, j + i, j0, np);
-                    out[(int64_t)g.kdim * (j0 - j_begin) + (int64_t)row * np + (j + i - j0)] =
-                        v[i];
-                }
-            }
-        }
+        for (int i = 0; i < PACK_VEC; ++i)
+            if (jl + i < j_count) dst[i] = v[i];
     }
 }
 
@@ -107,8 +84,9 @@ im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ out, int 
 // element read from L2 once per block instead of once per tap), then every (c, ky, kx)
 // packed row of the band is written as one contiguous run of TR*Q pixels: one LDS and one
 // coalesced STG per output element.  The kernel is HBM-write bound.
-//   SLICED = false: dst = cols[row][j]               (im2col_transform layout)
-//   SLICED = true : dst = slice buffer of the chunk  (band never crosses a slice)
+//   SLICED = false: dst = cols[row][j]                   (im2col_transform layout)
+//   SLICED = true : dst = slices[row][j - j_begin] of the chunk's (kdim x j_count) matrix
+//                   (blocks walk the chunk's slices; a band never crosses a slice)
 // ---------------------------------------------------------------------------------------
 constexpr int BAND_THREADS = 256;
 constexpr int BAND_MAXM = 8;  // pixels per band <= BAND_THREADS * BAND_MAXM
@@ -132,7 +110,7 @@ struct BandPlan {
 template <bool SLICED>
 __global__ void __launch_bounds__(BAND_THREADS)
 im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __restrict__ out,
-                   int band_rows, int first_slice, int64_t j_begin,
+                   int band_rows, int first_slice, int64_t j_begin, int64_t j_count,
                    const __grid_constant__ CUtensorMap tm_x) {
     extern __shared__ __align__(128) float smem_band[];  // [CC][IR][IWp][pixel tab][row tab]
     __shared__ __align__(8) uint64_t win_bar;
@@ -227,20 +205,8 @@ im2col_band_kernel(Geom g, BandPlan bp, const float* __restrict__ x, float* __re
     __syncthreads();
     if (bp.tma) ptx::mbar_wait(&win_bar, 0);
     // ---- destination of this band's run in every packed row ----
-    const int64_t jband = (int64_t)n * g.PQ + (int64_t)y_lo * g.Q;
-    int64_t row_stride, dst0;
-    if (!SLICED) {
-        row_stride = g.npix;
-        dst0 = jband;
-    } else {
-        const int per_img = (g.P + band_rows - 1) / band_rows;
-        const int s = first_slice + unit;
-        const int s0 = (s - (s / per_img) * per_img) * band_rows;
-        const int np = (min(g.P, s0 + band_rows) - s0) * g.Q;
-        const int64_t j0 = (int64_t)n * g.PQ + (int64_t)s0 * g.Q;
-        row_stride = np;
-        dst0 = (int64_t)g.kdim * (j0 - j_begin) + (jband - j0);
-    }
+    const int64_t row_stride = j_count;
+    const int64_t dst0 = (int64_t)n * g.PQ + (int64_t)y_lo * g.Q - j_begin;
     // ---- each warp streams 4 packed rows (c, ky, kx) per pass; one offset-table load
     //      feeds 4 gathers and 4 coalesced stores ----
     constexpr int NW = BAND_THREADS / 32;
@@ -339,7 +305,8 @@ static bool band_plan(const Geom& g, int max_rows, int64_t units, BandPlan* bp, 
 }
 
 int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
-                       int first_slice, int count, int64_t j_begin, cudaStream_t st) {
+                       int first_slice, int count, int64_t j_begin, int64_t j_count,
+                       cudaStream_t st) {
     BandPlan bp{};
     const int64_t units = sliced ? count : g.N;
     if (!band_plan(g, sliced ? band_rows : g.P, units, &bp, !sliced)) return CB_ERR_UNSUPPORTED;
@@ -375,7 +342,7 @@ int launch_im2col_band(const Geom& g, const float* x, float* out, bool sliced, i
         if (e != cudaSuccess) return fail(CB_ERR_CUDA, cudaGetErrorString(e));
     }
     kern<<<dim3((unsigned)gx, (unsigned)gy), BAND_THREADS, bp.smem, st>>>(
-        g, bp, x, out, band_rows, first_slice, j_begin, tm);
+        g, bp, x, out, band_rows, first_slice, j_begin, j_count, tm);
     return check_launch(sliced ? "sconv_pack_band" : "im2col_band");
 }
 
@@ -401,26 +368,6 @@ __global__ void weight_split_kernel(int rows, int kdim, int kdim_pad, const floa
     }
 }
 
-// K5: y[n, f, p] = bias[f] + acc[slice(j)][f][j - j0] for the pixels [j_begin, +j_count)
-__global__ void unpack_kernel(Geom g, int band_rows, int64_t j_begin, int64_t j_count,
-                              const float* __restrict__ acc, const float* __restrict__ bias,
-                              float* __restrict__ y) {
-    const int64_t total = j_count * g.K;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int f = (int)(i / j_count);
-        const int64_t j = j_begin + (i - (int64_t)f * j_count);
-        const int64_t n = j / g.PQ;
-        const int64_t p = j - n * g.PQ;
-        int64_t j0;
-        int np;
-        slice_of(g, band_rows, j, j0, np);
-        const float b = bias ? __ldg(bias + f) : 0.f;
-        y[(n * g.K + f) * g.PQ + p] =
-            b + __ldg(acc + (int64_t)g.K * (j0 - j_begin) + (int64_t)f * np + (j - j0));
-    }
-}
-
 // y (N, K, P*Q) = bias broadcast (or 0): the output initialisation of _alloc_output.
 __global__ void fill_bias_kernel(int64_t images, int K, int PQ, const float* __restrict__ bias,
                                  float* __restrict__ y) {
@@ -438,26 +385,17 @@ static int grid_for(int64_t total, int threads) {
     return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
-int launch_im2col(const Geom& g, const float* x, float* out, bool sliced, int band_rows,
-                  int64_t j_begin, int64_t j_count, cudaStream_t st) {
+int launch_im2col(const Geom& g, const float* x, float* out, int64_t j_begin, int64_t j_count,
+                  cudaStream_t st) {
     if (j_count == 0) return CB_OK;
     const int64_t col_blocks = ceil_div64(j_count, (int64_t)PACK_THREADS * PACK_VEC);
     const int64_t rows = (int64_t)g.C * g.RS;
     const int64_t blocks = rows * col_blocks;
     if (blocks > 0x7fffffffLL) return fail(CB_ERR_UNSUPPORTED, "im2col grid too large");
-    const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    if (!sliced) {
-        const bool vec_ok = aligned && (j_count % PACK_VEC == 0);
-        im2col_kernel<false><<<(unsigned)blocks, PACK_THREADS, 0, st>>>(
-            g, x, out, band_rows, j_begin, j_count, col_blocks, vec_ok);
-    } else {
-        // a VEC group never straddles a slice when slice starts are multiples of VEC
-        const bool vec_ok = aligned && (g.Q % PACK_VEC == 0) && (j_begin % PACK_VEC == 0) &&
-                            (j_count % PACK_VEC == 0);
-        im2col_kernel<true><<<(unsigned)blocks, PACK_THREADS, 0, st>>>(
-            g, x, out, band_rows, j_begin, j_count, col_blocks, vec_ok);
-    }
-    return check_launch(sliced ? "sconv_pack" : "im2col");
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (j_count % PACK_VEC == 0);
+    im2col_kernel<<<(unsigned)blocks, PACK_THREADS, 0, st>>>(g, x, out, j_begin, j_count,
+                                                             col_blocks, vec_ok);
+    return check_launch(j_begin || j_count != g.npix ? "sconv_pack" : "im2col");
 }
 
 int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float* w, void* hi,
@@ -502,11 +440,11 @@ int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, const float* 
 }
 
 // K5 by rows: a slice is a band of whole output rows of one image, so each (slice, channel)
-// pair is one contiguous run in both the accumulator buffer and y.  One warp per run, float4
+// pair is one contiguous run in both the accumulator matrix and y.  One warp per run, float4
 // when both ends are 16-byte aligned.
 __global__ void __launch_bounds__(256)
-unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int64_t nrows,
-                   const float* __restrict__ acc, const float* __restrict__ bias,
+unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int64_t j_count,
+                   int64_t nrows, const float* __restrict__ acc, const float* __restrict__ bias,
                    float* __restrict__ y) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -519,7 +457,7 @@ unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int6
     const int y0 = (int)(sg - n * per_img) * band_rows;
     const int np = min(band_rows, g.P - y0) * g.Q;
     const int64_t j0 = n * g.PQ + (int64_t)y0 * g.Q;
-    const float* src = acc + (int64_t)g.K * (j0 - j_begin) + (int64_t)f * np;
+    const float* src = acc + (int64_t)f * j_count + (j0 - j_begin);
     float* dst = y + (n * g.K + f) * g.PQ + (int64_t)y0 * g.Q;
     const float b = bias ? __ldg(bias + f) : 0.f;
     if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
@@ -559,27 +497,51 @@ unpack_rows_kernel(Geom g, int band_rows, int64_t s_first, int64_t j_begin, int6
     }
 }
 
-// K5 when every slice is a whole image (band_rows >= P): the chunk's accumulators
-// [image][channel][pixel] have exactly y's NCHW layout, so the unpack is a flat copy of the
-// chunk's images with the channel bias added.  float4 lanes, 4 vectors in flight per thread.
+// K5 when every slice is a whole image (band_rows >= P): image i of the chunk is the
+// column block acc[:, i*PQ : (i+1)*PQ] of the K x J accumulator matrix and y's images are
+// contiguous, so y is walked linearly in float4 lanes, 4 vectors in flight per thread; each
+// vector's (image, channel, pixel) advances by the grid stride in mixed radix (no division
+// in the loop).
 __global__ void __launch_bounds__(256)
-unpack_images_kernel(int64_t nvec, int pq4, int K, const float4* __restrict__ acc,
+unpack_images_kernel(int64_t nvec, int pq4, int K, int64_t j4, const float4* __restrict__ acc,
                      const float* __restrict__ bias, float4* __restrict__ y) {
     const int64_t stride = (int64_t)gridDim.x * 256;
-    for (int64_t v0 = blockIdx.x * 256LL + threadIdx.x; v0 < nvec; v0 += 4 * stride) {
+    const int64_t img4 = (int64_t)K * pq4;
+    // the stride and this thread's first vector in (image, channel, pixel) digits
+    const int64_t s_im = stride / img4;
+    const int s_f = (int)((stride - s_im * img4) / pq4);
+    const int s_p = (int)(stride - s_im * img4 - (int64_t)s_f * pq4);
+    int64_t i = blockIdx.x * 256LL + threadIdx.x;
+    int64_t im = i / img4;
+    int f = (int)((i - im * img4) / pq4);
+    int p = (int)(i - im * img4 - (int64_t)f * pq4);
+    auto advance = [&] {
+        i += stride;
+        p += s_p;
+        f += s_f;
+        im += s_im;
+        if (p >= pq4) { p -= pq4; ++f; }
+        if (f >= K) { f -= K; ++im; }
+    };
+    while (i < nvec) {
         float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (v0 + u * stride < nvec) v[u] = __ldcs(acc + v0 + u * stride);
+        int fu[4];
+        int64_t iu[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int64_t i = v0 + u * stride;
-            if (i >= nvec) break;
+            iu[u] = i;
+            fu[u] = f;
+            if (i < nvec) v[u] = __ldcs(acc + (int64_t)f * j4 + im * pq4 + p);
+            advance();
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (iu[u] >= nvec) break;
             if (bias) {
-                const float b = __ldg(bias + (int)((i / pq4) % K));
+                const float b = __ldg(bias + fu[u]);
                 v[u].x += b, v[u].y += b, v[u].z += b, v[u].w += b;
             }
-            y[i] = v[u];
+            y[iu[u]] = v[u];
         }
     }
 }
@@ -594,7 +556,7 @@ int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count
         const int64_t nvec = total / 4;
         const int64_t blocks = std::min<int64_t>((nvec + 1023) / 1024, (int64_t)sm_count() * 8);
         unpack_images_kernel<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, st>>>(
-            nvec, g.PQ / 4, g.K, reinterpret_cast<const float4*>(acc), bias,
+            nvec, g.PQ / 4, g.K, j_count / 4, reinterpret_cast<const float4*>(acc), bias,
             reinterpret_cast<float4*>(y + (j_begin / g.PQ) * (int64_t)g.K * g.PQ));
         return check_launch("unpack_images");
     }
@@ -613,8 +575,8 @@ int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count
     const int64_t nrows = nslices * g.K;
     const int64_t blocks = (nrows + 7) / 8;
     if (blocks > 0x7fffffffLL) return fail(CB_ERR_UNSUPPORTED, "unpack grid too large");
-    unpack_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, band_rows, s_first, j_begin, nrows,
-                                                          acc, bias, y);
+    unpack_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, band_rows, s_first, j_begin, j_count,
+                                                          nrows, acc, bias, y);
     return check_launch("unpack");
 }
 

@@ -116,8 +116,11 @@ def test_slice_pack_is_im2col_columns():
     oh, ow = orc.output_shape(d)
     cols = orc.im2col(d, x)
     whole = orc.slice_pack(d, x, oh, 0, d.batch)  # one slice per image
-    assert np.array_equal(whole[: cols.shape[0] * oh * ow].reshape(cols.shape[0], oh * ow),
-                          cols[:, : oh * ow])
+    assert np.array_equal(whole.reshape(cols.shape), cols)
+    # 2-row bands (3 per image): slices 1..3 = image 0 rows 2-4 and image 1 rows 0-1, one
+    # column block across the image boundary
+    part = orc.slice_pack(d, x, 2, 1, 3)
+    assert np.array_equal(part.reshape(cols.shape[0], -1), cols[:, 2 * ow: oh * ow + 2 * ow])
 
 
 def test_parity_metrics():
