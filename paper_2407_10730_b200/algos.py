@@ -35,7 +35,7 @@ from __future__ import annotations
 import ctypes
 import os
 import functools
-from dataclasses import dataclass, fields
+from dataclasses import dataclass, field, fields
 
 import numpy as np
 
@@ -295,6 +295,20 @@ class _Prep:
     ow: int
     kdim: int            # (C/g)*R*S
     kpad: int            # split width of the weight rows (stepwise variants)
+    # tile plans by pixel count (cb_plan_tiles, pure host arithmetic of the descriptor):
+    # IN_TILING computes a plan once and then looks it up
+    tiles: dict = field(default_factory=dict, compare=False, hash=False)
+    # SConv plans by CacheParams (None: the default budget): (plan, cb_slice_plan struct)
+    sconv: dict = field(default_factory=dict, compare=False, hash=False)
+
+
+def _tile_plan(pr: _Prep, pixels: int):
+    tp = pr.tiles.get(pixels)
+    if tp is None:
+        tp = _capi.CbTilePlan()
+        _capi.check(_capi.load().cb_plan_tiles(pr.vid, pr.pcd, pixels, ctypes.byref(tp)))
+        pr.tiles[pixels] = tp
+    return tp
 
 
 @functools.lru_cache(maxsize=4096)
@@ -465,13 +479,12 @@ def conv_baseline_im2col_gemm(inputs, ledger, blocking: GemmBlocking | None = No
                        dtype=torch.float32, device=x.device)
     w_hi, w_lo, w_f32 = _weight_buffers(w, d, variant, pr)
     st = _stream()
-    tp = _capi.CbTilePlan()
     with _phase(ledger, Phase.PRE_REORDER):
         _capi.check(lib.cb_im2col_f32(pr.pcd, x.data_ptr(), cols.data_ptr(), st))
     with _phase(ledger, Phase.IN_PACKING):
         _split_into(lib, pr, d, w, w_hi, w_lo, st)
     with _phase(ledger, Phase.IN_TILING):
-        _capi.check(lib.cb_plan_tiles(pr.vid, pr.pcd, 0, ctypes.byref(tp)))
+        _tile_plan(pr, 0)
     with _phase(ledger, Phase.IN_MICROKERNEL):
         _capi.check(lib.cb_conv_gemm_cols(pr.vid, pr.pcd, cols.data_ptr(), _ptr(w_hi), _ptr(w_lo),
                                           _ptr(w_f32), _ptr(b), y.data_ptr(), st))
@@ -489,9 +502,17 @@ class SConvPlan:
     max_chunk_pixels: int
 
 
-@functools.lru_cache(maxsize=4096)
-def _plan_sconv_cached(desc: ConvDescriptor, cache: CacheParams) -> SConvPlan:
-    return plan_sconv(desc, cache)
+def _sconv_plan(pr: _Prep, desc, cache: CacheParams | None):
+    """(plan, its cb_slice_plan struct), planned once per descriptor and CacheParams."""
+    try:
+        got = pr.sconv.get(cache)
+    except TypeError:  # an unhashable caller-side CacheParams
+        plan = plan_sconv(desc, cache)
+        return plan, _capi.CbSlicePlan(plan.band_rows, plan.num_slices)
+    if got is None:
+        plan = plan_sconv(desc, cache)
+        got = pr.sconv[cache] = (plan, _capi.CbSlicePlan(plan.band_rows, plan.num_slices))
+    return got
 
 
 def plan_sconv(desc, cache: CacheParams | None = None) -> SConvPlan:
@@ -549,13 +570,8 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
     y = torch.empty((d.batch, d.out_channels, pr.oh, pr.ow), dtype=torch.float32, device=x.device)
     w_hi, w_lo, w_f32 = _weight_buffers(w, d, variant, pr)
     st = _stream()
-    tp = _capi.CbTilePlan()
     with _phase(ledger, Phase.PRE_ANALYSIS):
-        try:
-            plan = _plan_sconv_cached(_norm(d), cache)
-        except TypeError:  # an unhashable caller-side CacheParams
-            plan = plan_sconv(d, cache)
-        sp = _capi.CbSlicePlan(plan.band_rows, plan.num_slices)
+        plan, sp = _sconv_plan(pr, d, cache)
     slices = torch.empty(pr.kdim * plan.max_chunk_pixels, dtype=torch.float32, device=x.device)
     acc = torch.empty(d.out_channels * plan.max_chunk_pixels, dtype=torch.float32,
                       device=x.device)
@@ -566,7 +582,7 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
     hp, lp, fp, bp = _ptr(w_hi), _ptr(w_lo), _ptr(w_f32), _ptr(b)
     for first, cnt, _jb, jc in plan.chunks:
         with _phase(ledger, Phase.IN_TILING):
-            _capi.check(lib.cb_plan_tiles(pr.vid, pr.pcd, jc, ctypes.byref(tp)))
+            _tile_plan(pr, jc)
         with _phase(ledger, Phase.IN_PACKING):
             _capi.check(lib.cb_sconv_pack_f32(pr.pcd, psp, first, cnt, xp, sl, st))
         with _phase(ledger, Phase.IN_MICROKERNEL):

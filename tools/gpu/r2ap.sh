@@ -1,0 +1,10 @@
+# After the SConv chunk-matrix layout and the cached host plans: GPU tests, the bench table,
+# then the full config-5 sweep on make_inputs data with CPU-oracle parity on every op, the
+# reference convbench report and the speedup chart.
+set -o pipefail
+mkdir -p gpurun_out/r2ap
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r2ap/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2ap/pytest.log
+timeout 900 python bench.py --no-cpu-baseline --no-variants > gpurun_out/r2ap/bench.json 2> gpurun_out/r2ap/bench.err; echo "bench rc=$?"
+timeout 3000 python tests/sweep_parity.py --warmups 1 --runs 3 --pending 24 --out gpurun_out/r2ap/sweep9243 > gpurun_out/r2ap/sweep.log 2>&1; echo "sweep rc=$?"; tail -3 gpurun_out/r2ap/sweep.log
+PYTHONPATH=baseline/_ref timeout 300 python -m convbench.cli report --main gpurun_out/r2ap/sweep9243/results_main.csv --baseline gpurun_out/r2ap/sweep9243/results_baseline.csv --out-speedup gpurun_out/r2ap/sweep9243/ref_speedup.csv --out-breakdown gpurun_out/r2ap/sweep9243/ref_breakdown.csv --out-summary gpurun_out/r2ap/sweep9243/ref_summary.json > gpurun_out/r2ap/report.log 2>&1; echo "report rc=$?"; tail -3 gpurun_out/r2ap/report.log
+python tools/charts.py speedup --in gpurun_out/r2ap/sweep9243/ref_speedup.csv --out gpurun_out/r2ap/sweep9243/speedup.svg --sort by-speedup --log-y; echo "chart rc=$?"
