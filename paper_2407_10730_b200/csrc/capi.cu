@@ -132,8 +132,8 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
                    const float* bias, float* y, cudaStream_t st);
 int ts_plan_query(const Geom& g, cb_tile_plan* out);
 int ts_weight_kdim(const Geom& g, int* pair, int* pf);
-int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, const float* w, void* hi, void* lo,
-                              cudaStream_t st);
+int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, int mixed, const float* w, void* hi,
+                              void* lo, cudaStream_t st);
 int ffma_plan_query(const Geom& g, int64_t npix, bool allow_split, cb_tile_plan* out);
 int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
               const void* w_lo, const float* bias, float* out, int add_mode, int zero_kind,
@@ -546,7 +546,7 @@ int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, vo
     if (L.ts) {  // K7: plain split rows, or the pair layout with one pad tap per (c, r) row
         int pair = 0, pf = 0;
         const int kd = ts_weight_kdim(g, &pair, &pf);
-        if (pair) return launch_weight_split_pairs(g, pf, cb_split_kdim(kd), w, w_hi, w_lo, (cudaStream_t)stream);
+        if (pair) return launch_weight_split_pairs(g, pf, cb_split_kdim(kd), pair == 2, w, w_hi, w_lo, (cudaStream_t)stream);
     }
     return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
                                (cudaStream_t)stream);

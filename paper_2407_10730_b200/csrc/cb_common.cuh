@@ -214,4 +214,33 @@ __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
     return __uint_as_float(((uint32_t)b) << 16);
 }
 
+// ------------------------------------------------------------------------------------
+// K7 "mixed" reduction layout (odd S = 2h + 1, even horizontal stride): every (c, r) row
+// cr contributes h tap pairs -- (pf, pf + 1), (pf + 2, pf + 3), ... -- each one 8-byte
+// aligned LDS.64 of two adjacent window columns, and one single tap (s = S - 1 when
+// pf = 0, s = 0 when pf = 1).  Rows are laid out two at a time: the pairs of row 2j, the
+// pairs of row 2j + 1, then the two singles as one more k pair, 2S elements per row pair
+// with no padding; an odd last row is followed by one zero element.  Shared by the A
+// producer (conv_ts.cu) and the weight packer (pack_kernels.cu).
+//   mixed_kdim = NR * S + (NR & 1);  mixed_map(k) -> row cr and tap s, or cr = -1 (zero)
+// ------------------------------------------------------------------------------------
+struct MixedTap {
+    int cr, s;
+};
+__host__ __device__ constexpr int mixed_kdim(int nr, int S) { return nr * S + (nr & 1); }
+__host__ __device__ constexpr MixedTap mixed_map(int k, int nr, int S, int pf) {
+    const int h2 = S - 1;  // pair elements of one row
+    const int rp = k / (2 * S), o = k - rp * 2 * S;
+    const int single = pf ? 0 : S - 1;
+    if (2 * rp + 1 < nr) {
+        if (o < h2) return {2 * rp, o + pf};
+        if (o < 2 * h2) return {2 * rp + 1, o - h2 + pf};
+        return {2 * rp + (o - 2 * h2), single};
+    }
+    if (2 * rp >= nr) return {-1, 0};
+    if (o < h2) return {nr - 1, o + pf};
+    if (o == h2) return {nr - 1, single};
+    return {-1, 0};
+}
+
 }  // namespace cb

@@ -31,7 +31,13 @@ namespace cb {
 
 constexpr int TS_BM = 128;
 #ifndef CB_TS_KPARTS
-#define CB_TS_KPARTS 3
+#define CB_TS_KPARTS 1
+#endif
+#ifndef CB_TS_DEPTH
+#define CB_TS_DEPTH 3  // 8-element groups of window loads in flight ahead of the split
+#endif
+#ifndef CB_TS_STW
+#define CB_TS_STW 1  // 8-element groups per tcgen05.st (1, 2 or 4: .x4 / .x8 / .x16)
 #endif
 constexpr int TS_PROD_WARPS = 4 * CB_TS_KPARTS;  // CB_TS_KPARTS per TMEM lane quadrant
 constexpr int TS_EPI_WARP0 = TS_PROD_WARPS;
@@ -169,11 +175,13 @@ __device__ __forceinline__ void load_pair(int k, uint32_t xs, uint32_t xa, uint3
 template <int C, int R, int S, int G0, int G1>
 __device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint32_t rstride,
                                             uint32_t a_hi, uint32_t a_lo, bool swap) {
-    constexpr int NG = G1 - G0, D = 3;
+    constexpr int NG = G1 - G0, D = CB_TS_DEPTH;
     // swap (even horizontal stride): lanes 16..31 load the second tap of an adjacent pair
     // first, so the warp's 32 addresses (2 words apart per pixel) cover all 32 banks
     const uint32_t xa = xs + (swap ? 4u : 0u), xb = xs + (swap ? 0u : 4u);
+    constexpr int W = CB_TS_STW;
     float v[D + 1][8];
+    uint32_t hv[4 * W], lv[4 * W];
 #pragma unroll
     for (int step = 0; step < NG + D; ++step) {
         if (step < NG) {
@@ -185,11 +193,13 @@ __device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint3
         if (step >= D) {
             const int gi = step - D;
             const float* u = v[gi % (D + 1)];
-            uint32_t hv[4], lv[4];
+            const int slot = gi % W;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) split_pair(u[2 * e], u[2 * e + 1], hv[e], lv[e]);
-            ptx::tmem_st_32x32b_x4(a_hi + (G0 + gi) * 4, hv);
-            ptx::tmem_st_32x32b_x4(a_lo + (G0 + gi) * 4, lv);
+            for (int e = 0; e < 4; ++e) split_pair(u[2 * e], u[2 * e + 1], hv[slot * 4 + e], lv[slot * 4 + e]);
+            if (slot == W - 1 || gi == NG - 1) {  // W groups (or the rest) per tcgen05.st
+                ptx::tmem_st_32x32b_groups(a_hi + (G0 + gi - slot) * 4, hv, slot + 1);
+                ptx::tmem_st_32x32b_groups(a_lo + (G0 + gi - slot) * 4, lv, slot + 1);
+            }
         }
     }
 }
@@ -199,8 +209,10 @@ __device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint3
 template <int C, int R, int S, int G0, int G1>
 __device__ __forceinline__ void build_pairs(uint32_t xs_pair, uint32_t cstride, uint32_t rstride,
                                             uint32_t a_hi, uint32_t a_lo) {
-    constexpr int SP = S + 1, KD = C * R * SP, NG = G1 - G0, D = 3;
+    constexpr int SP = S + 1, KD = C * R * SP, NG = G1 - G0, D = CB_TS_DEPTH;
+    constexpr int W = CB_TS_STW;
     float2 v[D + 1][4];
+    uint32_t hv[4 * W], lv[4 * W];
 #pragma unroll
     for (int step = 0; step < NG + D; ++step) {
         if (step < NG) {
@@ -220,13 +232,70 @@ __device__ __forceinline__ void build_pairs(uint32_t xs_pair, uint32_t cstride, 
         }
         if (step >= D) {
             const int gi = step - D;
-            uint32_t hv[4], lv[4];
+            const int slot = gi % W;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) split_pair(v[gi % (D + 1)][e].x, v[gi % (D + 1)][e].y, hv[e], lv[e]);
-            ptx::tmem_st_32x32b_x4(a_hi + (G0 + gi) * 4, hv);
-            ptx::tmem_st_32x32b_x4(a_lo + (G0 + gi) * 4, lv);
+            for (int e = 0; e < 4; ++e)
+                split_pair(v[gi % (D + 1)][e].x, v[gi % (D + 1)][e].y, hv[slot * 4 + e], lv[slot * 4 + e]);
+            if (slot == W - 1 || gi == NG - 1) {  // W groups (or the rest) per tcgen05.st
+                ptx::tmem_st_32x32b_groups(a_hi + (G0 + gi - slot) * 4, hv, slot + 1);
+                ptx::tmem_st_32x32b_groups(a_lo + (G0 + gi - slot) * 4, lv, slot + 1);
+            }
         }
     }
+}
+
+// Mixed-layout producer (cb_common.cuh: mixed_map): groups [G0, G1) of 8 elements; a k pair
+// inside a row's pair region is one LDS.64, the pair of two rows' single taps two LDS.32.
+template <int C, int R, int S, int PF, int G0, int G1>
+__device__ __forceinline__ void build_mixed(uint32_t xs, uint32_t cstride, uint32_t rstride,
+                                            uint32_t a_hi, uint32_t a_lo) {
+    constexpr int NR = C * R, NG = G1 - G0, D = CB_TS_DEPTH;
+    constexpr int W = CB_TS_STW;
+    float2 v[D + 1][4];
+    uint32_t hv[4 * W], lv[4 * W];
+#pragma unroll
+    for (int step = 0; step < NG + D; ++step) {
+        if (step < NG) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = (G0 + step) * 8 + 2 * e;
+                const MixedTap t0 = mixed_map(k, NR, S, PF), t1 = mixed_map(k + 1, NR, S, PF);
+                float2& d = v[step % (D + 1)][e];
+                if (t0.cr >= 0 && t1.cr == t0.cr && t1.s == t0.s + 1) {  // aligned tap pair
+                    const uint32_t a = xs + (t0.cr / R) * cstride + (t0.cr % R) * rstride + 4 * t0.s;
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d.x), "=f"(d.y) : "r"(a));
+                } else {
+                    d.x = t0.cr >= 0 ? lds_f32(xs + (t0.cr / R) * cstride + (t0.cr % R) * rstride + 4 * t0.s) : 0.f;
+                    d.y = t1.cr >= 0 ? lds_f32(xs + (t1.cr / R) * cstride + (t1.cr % R) * rstride + 4 * t1.s) : 0.f;
+                }
+            }
+        }
+        if (step >= D) {
+            const int gi = step - D;
+            const int slot = gi % W;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                split_pair(v[gi % (D + 1)][e].x, v[gi % (D + 1)][e].y, hv[slot * 4 + e], lv[slot * 4 + e]);
+            if (slot == W - 1 || gi == NG - 1) {  // W groups (or the rest) per tcgen05.st
+                ptx::tmem_st_32x32b_groups(a_hi + (G0 + gi - slot) * 4, hv, slot + 1);
+                ptx::tmem_st_32x32b_groups(a_lo + (G0 + gi - slot) * 4, lv, slot + 1);
+            }
+        }
+    }
+}
+
+template <int C, int R, int S, int PF>
+__device__ __forceinline__ void build_mixed_part(int kpart, uint32_t xs, uint32_t cstride,
+                                                 uint32_t rstride, uint32_t a_hi, uint32_t a_lo) {
+    constexpr int G = (mixed_kdim(C * R, S) + 7) / 8, P = CB_TS_KPARTS;
+    if (kpart == 0)
+        build_mixed<C, R, S, PF, 0, G * 1 / P>(xs, cstride, rstride, a_hi, a_lo);
+    else if (kpart == 1 && P > 1)
+        build_mixed<C, R, S, PF, G * 1 / P, G * 2 / P>(xs, cstride, rstride, a_hi, a_lo);
+    else if (kpart == 2 && P > 2)
+        build_mixed<C, R, S, PF, G * 2 / P, G * 3 / P>(xs, cstride, rstride, a_hi, a_lo);
+    else if (P > 3)
+        build_mixed<C, R, S, PF, G * 3 / P, G>(xs, cstride, rstride, a_hi, a_lo);
 }
 
 template <int C, int R, int S>
@@ -235,9 +304,9 @@ __device__ __forceinline__ void build_pairs_part(int kpart, uint32_t xs_pair, ui
     constexpr int G = (C * R * (S + 1) + 7) / 8, P = CB_TS_KPARTS;
     if (kpart == 0)
         build_pairs<C, R, S, 0, G * 1 / P>(xs_pair, cstride, rstride, a_hi, a_lo);
-    else if (kpart == 1)
+    else if (kpart == 1 && P > 1)
         build_pairs<C, R, S, G * 1 / P, G * 2 / P>(xs_pair, cstride, rstride, a_hi, a_lo);
-    else if (kpart == 2)
+    else if (kpart == 2 && P > 2)
         build_pairs<C, R, S, G * 2 / P, G * 3 / P>(xs_pair, cstride, rstride, a_hi, a_lo);
     else if (P > 3)
         build_pairs<C, R, S, G * 3 / P, G>(xs_pair, cstride, rstride, a_hi, a_lo);
@@ -251,9 +320,9 @@ __device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_
     constexpr int G = (C * R * S + 7) / 8, P = CB_TS_KPARTS;
     if (kpart == 0)
         build_fixed<C, R, S, 0, G * 1 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
-    else if (kpart == 1)
+    else if (kpart == 1 && P > 1)
         build_fixed<C, R, S, G * 1 / P, G * 2 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
-    else if (kpart == 2)
+    else if (kpart == 2 && P > 2)
         build_fixed<C, R, S, G * 2 / P, G * 3 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
     else if (P > 3)
         build_fixed<C, R, S, G * 3 / P, G>(xs, cstride, rstride, a_hi, a_lo, swap);
@@ -276,7 +345,7 @@ CB_TS_FIXED_LIST(CB_TS_LAYOUT)
 // One instantiation per (CTA group, compile-time layout FX, pair mode): each kernel holds
 // only its own unrolled producer -- with all layouts in one kernel the ncu profile showed
 // 12% of warp stalls as no_instructions (instruction-cache misses).
-template <int CG, int FX, bool PAIR>
+template <int CG, int FX, int MODE>  // MODE: 0 plain, 1 padded pairs, 2 / 3 mixed layout with pf = 0 / 1
 __global__ void __launch_bounds__(TS_THREADS, 1)
 conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUtensorMap tm_x,
                const __grid_constant__ CUtensorMap tm_whi, const __grid_constant__ CUtensorMap tm_wlo,
@@ -314,10 +383,10 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         ptx::mbar_init(w_full, 1);
         for (int b = 0; b < p.nwin; ++b) {
             ptx::mbar_init(&s_full[b], 1);
-            ptx::mbar_init(&s_empty[b], 32 * TS_PROD_WARPS);
+            ptx::mbar_init(&s_empty[b], TS_PROD_WARPS);
         }
         for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&a_full[b], CG * 32 * TS_PROD_WARPS);
+            ptx::mbar_init(&a_full[b], CG * TS_PROD_WARPS);
             ptx::mbar_init(&a_empty[b], 1);
             ptx::mbar_init(&acc_full[b], 1);
             ptx::mbar_init(&acc_empty[b], CG * 128);
@@ -370,13 +439,12 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         const uint32_t lane_addr = tmem_base + ((uint32_t)(quad * 32) << 16);
         const int nchunks = p.kp / 32;
         const bool swap = (g.sw % 2 == 0) && lane >= 16 && !(p.debug & 32);
-        int i = 0;
-        int ws = 0;  // staging-window ring slot and phase
-        uint32_t wph = 0;
-        for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles; tw.next(p), ++i) {
-            const int b = i & 1;
-            const uint32_t ph = (i >> 1) & 1;
-            const int n = tw.n;
+        // The tile loop is software-pipelined across tiles: the next tile's window origin and
+        // the (non-blocking) tests of its two barriers are issued before this tile's
+        // tcgen05.st drain, so their latencies (~250-400 cycles a tile when taken in
+        // sequence at the top of the loop) overlap the drain and the hand-off.  One lane per
+        // warp arrives (after __syncwarp) instead of 32.
+        auto window_origin = [&](const TileWalk& tw, int ws) -> uint32_t {
             // this CTA's first pixel; past the image (the second half of a pair's last tile)
             // the window origin stays inside it and nothing is stored
             const int p0 = min(tw.ti * (TS_BM * CG) + (int)rank * TS_BM, g.PQ - 1);
@@ -384,19 +452,30 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             const int pix = min(p0 + m, g.PQ - 1);  // rows past the image: finite, never stored
             const int oy = div_q(pix, p);
             const int ox = pix - oy * g.Q;
-            const uint32_t xs = ptx::smem_u32(stage0) + ws * p.stage_stride +
-                                4u * (uint32_t)((oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw));
+            return ptx::smem_u32(stage0) + ws * p.stage_stride +
+                   4u * (uint32_t)((oy - oy_a) * g.sh * p.box_w + ox * g.sw + (p.x0 - g.pw));
+        };
+        int i = 0;
+        int ws = 0;  // staging-window ring slot and phase
+        uint32_t wph = 0;
+        TileWalk tw(p, unit0, nunits);
+        bool have = tw.t < p.total_tiles;
+        uint32_t xs = 0;
+        if (have) {
+            xs = window_origin(tw, ws);
             ptx::mbar_wait(&s_full[ws], wph);
-            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 1 : 11, i);
-            ptx::mbar_wait(&a_empty[b], ph ^ 1);
+            ptx::mbar_wait(&a_empty[0], 1);
             ptx::tc_fence_after();
+        }
+        while (have) {
+            const int b = i & 1;
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 2 : 12, i);
             const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
             const uint32_t a_lo = a_hi + half_cols;
             if (FX != 0 && !(p.debug & 16)) {
                 if (i < 2) {  // columns past the written groups: zero once per A buffer
                     const uint32_t z[4] = {0u, 0u, 0u, 0u};
-                    const int kd = PAIR ? g.C * g.R * (g.S + 1) : g.kdim;
+                    const int kd = MODE == 1 ? g.C * g.R * (g.S + 1) : MODE >= 2 ? mixed_kdim(g.C * g.R, g.S) : g.kdim;
                     for (int c4 = ((kd + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
                         ptx::tmem_st_32x32b_x4(a_hi + c4, z);
                         ptx::tmem_st_32x32b_x4(a_lo + c4, z);
@@ -404,10 +483,12 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 }
                 const uint32_t cstride = 4u * p.box_rows * p.box_w, rstride = 4u * g.dh * p.box_w;
                 using L = TsLayout<FX>;
-                if constexpr (FX != 0 && PAIR && L::S % 2 == 1) {
+                if constexpr (FX != 0 && MODE >= 2 && L::S % 2 == 1) {
+                    build_mixed_part<L::C, L::R, L::S, MODE - 2>(kpart, xs, cstride, rstride, a_hi, a_lo);
+                } else if constexpr (FX != 0 && MODE == 1 && L::S % 2 == 1) {
                     const uint32_t xs_pair = xs - 4u * p.pf;  // 8-byte aligned (plan_ts)
                     build_pairs_part<L::C, L::R, L::S>(kpart, xs_pair, cstride, rstride, a_hi, a_lo);
-                } else if constexpr (FX != 0 && !PAIR) {
+                } else if constexpr (FX != 0 && MODE == 0) {
                     build_fixed_part<L::C, L::R, L::S>(kpart, xs, cstride, rstride, a_hi, a_lo, swap);
                 }
             }
@@ -433,17 +514,38 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 }
             }
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 3 : 13, i);
-            ptx::tmem_st_wait();
-            ptx::tc_fence_before();
-            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 4 : 14, i);
-            if (CG == 2)
-                ptx::mbar_arrive_remote(a_full_l0 + b * sizeof(uint64_t));
-            else
-                ptx::mbar_arrive(&a_full[b]);
-            ptx::mbar_arrive(&s_empty[ws]);
+            // the next tile: origin and barrier tests, in flight over this tile's drain
+            const int ws_cur = ws;
+            tw.next(p);
+            ++i;
             if (++ws == p.nwin) {
                 ws = 0;
                 wph ^= 1;
+            }
+            have = tw.t < p.total_tiles;
+            const uint32_t aph = ((i >> 1) & 1) ^ 1;
+            bool s_ok = true, a_ok = true;
+            if (have) {
+                xs = window_origin(tw, ws);
+                s_ok = ptx::mbar_test(&s_full[ws], wph);
+                a_ok = ptx::mbar_test(&a_empty[i & 1], aph);
+            }
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 4 : 14, i - 1);
+            if (lane == 0) {
+                if (CG == 2)
+                    ptx::mbar_arrive_remote(a_full_l0 + b * sizeof(uint64_t));
+                else
+                    ptx::mbar_arrive(&a_full[b]);
+                ptx::mbar_arrive(&s_empty[ws_cur]);
+            }
+            if (have) {
+                if (!s_ok) ptx::mbar_wait(&s_full[ws], wph);
+                if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 1 : 11, i);
+                if (!a_ok) ptx::mbar_wait(&a_empty[i & 1], aph);
+                ptx::tc_fence_after();
             }
         }
     } else if (warp < TS_TMA_WARP) {
@@ -518,21 +620,25 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         // ============================ TMA: weights once, then input windows =============
         const uint32_t leader = ptx::elect_one();
         const int wblocks = p.kb_w / 64;
-        if (leader) {  // this CTA's weight rows [rank * w_rows, +w_rows); pairs: leader barrier
-            if (rank == 0) ptx::mbar_arrive_expect_tx(w_full, CG * 2 * p.w_half_bytes);
-            const int row0 = (int)rank * p.w_rows;
-            for (int kb = 0; kb < wblocks; ++kb) {
-                uint8_t* dh = w_hi + (size_t)kb * p.w_rows * 128;
-                uint8_t* dl = w_lo + (size_t)kb * p.w_rows * 128;
-                if (CG == 2) {
-                    ptx::tma_load_2d_pair(dh, &tm_whi, ptx::leader_bar(w_full), kb * 64, row0);
-                    ptx::tma_load_2d_pair(dl, &tm_wlo, ptx::leader_bar(w_full), kb * 64, row0);
-                } else {
-                    ptx::tma_load_2d(dh, &tm_whi, w_full, kb * 64, row0);
-                    ptx::tma_load_2d(dl, &tm_wlo, w_full, kb * 64, row0);
+        // the weights are issued after the first window: the window heads the first tile's
+        // chain (build -> MMA), the weights are first needed at the MMAs
+        auto load_weights = [&]() {
+            if (leader) {  // this CTA's weight rows [rank * w_rows, +w_rows); pairs: leader barrier
+                if (rank == 0) ptx::mbar_arrive_expect_tx(w_full, CG * 2 * p.w_half_bytes);
+                const int row0 = (int)rank * p.w_rows;
+                for (int kb = 0; kb < wblocks; ++kb) {
+                    uint8_t* dh = w_hi + (size_t)kb * p.w_rows * 128;
+                    uint8_t* dl = w_lo + (size_t)kb * p.w_rows * 128;
+                    if (CG == 2) {
+                        ptx::tma_load_2d_pair(dh, &tm_whi, ptx::leader_bar(w_full), kb * 64, row0);
+                        ptx::tma_load_2d_pair(dl, &tm_wlo, ptx::leader_bar(w_full), kb * 64, row0);
+                    } else {
+                        ptx::tma_load_2d(dh, &tm_whi, w_full, kb * 64, row0);
+                        ptx::tma_load_2d(dl, &tm_wlo, w_full, kb * 64, row0);
+                    }
                 }
             }
-        }
+        };
         __syncwarp();
         int i = 0;
         int ws = 0;  // staging-window ring slot and phase
@@ -550,12 +656,14 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 ptx::tma_load_4d(reinterpret_cast<uint8_t*>(stage0) + (size_t)ws * p.stage_stride, &tm_x,
                                  &s_full[ws], -p.x0, iy0, 0, n);
             }
+            if (i == 0) load_weights();
             __syncwarp();
             if (++ws == p.nwin) {
                 ws = 0;
                 wph ^= 1;
             }
         }
+        if (i == 0) load_weights();  // a CTA without tiles (not launched by launch_conv_ts)
     } else {
         // ============================ MMA issuer ========================================
         const uint32_t leader = ptx::elect_one();
@@ -623,13 +731,17 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
 using TsKernel = void (*)(const TsParams, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                          const CUtensorMap);
 template <int CG>
-static TsKernel ts_kernel_for(int fixed, bool pair) {
+static TsKernel ts_kernel_for(int fixed, int mode) {
     switch (fixed) {
-#define CB_TS_K(id, c, r, s) \
-    case id: return pair ? conv_ts_kernel<CG, id, true> : conv_ts_kernel<CG, id, false>;
+#define CB_TS_K(id, c, r, s)                                       \
+    case id:                                                       \
+        return mode == 3   ? conv_ts_kernel<CG, id, 3>             \
+               : mode == 2 ? conv_ts_kernel<CG, id, 2>             \
+               : mode == 1 ? conv_ts_kernel<CG, id, 1>             \
+                           : conv_ts_kernel<CG, id, 0>;
         CB_TS_FIXED_LIST(CB_TS_K)
 #undef CB_TS_K
-        default: return conv_ts_kernel<CG, 0, false>;
+        default: return conv_ts_kernel<CG, 0, 0>;
     }
 }
 
@@ -661,24 +773,31 @@ static TsPlan plan_ts(const Geom& g) {
     pl.x0 = round_up(g.pw, 4);  // 16-byte aligned window start
     // pair mode: compile-time producer, even horizontal stride, odd S, the padded reduction
     // fits TMEM next to two accumulators
+    // (2: the mixed layout -- tap pairs plus one single tap per row, no padding; 1: padded
+    // pairs, kept for A/B runs with CB_TS_PAIRMODE=1)
     pl.pair = 0;
     pl.pf = (pl.x0 - g.pw) & 1;
-    const int kd_pair = g.C * g.R * (g.S + 1);
-    static const bool no_pair = std::getenv("CB_TS_NO_PAIR") != nullptr;
-    if (!no_pair && ts_fixed_id(g) && g.S % 2 == 1 && g.sw % 2 == 0 &&
+    static const int pair_mode = [] {
+        const char* e = std::getenv("CB_TS_PAIRMODE");
+        return std::getenv("CB_TS_NO_PAIR") ? 0 : e ? std::atoi(e) : 2;
+    }();
+    const int kd_pair = pair_mode == 2 ? mixed_kdim(g.C * g.R, g.S) : g.C * g.R * (g.S + 1);
+    if (pair_mode && ts_fixed_id(g) && g.S % 2 == 1 && g.sw % 2 == 0 &&
         2 * pl.n_pad + 2 * round_up(kd_pair, 32) <= TS_TMEM_COLS)
-        pl.pair = 1;
+        pl.pair = pair_mode == 2 ? 2 : 1;
     pl.kdim = pl.pair ? kd_pair : g.kdim;
     pl.kp = round_up(pl.kdim, 32);
     pl.kb_w = round_up(pl.kdim, 64);  // == cb_split_kdim(kdim)
     if (pl.n_pad > 256 || 2 * pl.n_pad + 2 * pl.kp > TS_TMEM_COLS) return pl;
     // window columns: every tap of every output column (+ the pad tap past the last one)
-    const int need = (g.Q - 1) * g.sw + (pl.x0 - g.pw) + (g.S - 1) * g.dw + 1 + (pl.pair && !pl.pf ? 1 : 0);
+    const int need = (g.Q - 1) * g.sw + (pl.x0 - g.pw) + (g.S - 1) * g.dw + 1 + (pl.pair == 1 && !pl.pf ? 1 : 0);
     pl.box_w = round_up(std::max(g.W + g.pw + pl.x0, need), 4);
     const int out_rows = std::min(g.P, (TS_BM - 1) / std::max(1, g.Q) + 2);
     pl.box_rows = (out_rows - 1) * g.sh + (g.R - 1) * g.dh + 1;
     if (pl.box_w > 256 || pl.box_rows > 256 || g.C > 256 || (g.W % 4) != 0) return pl;
-    pl.stage_bytes = (uint32_t)g.C * pl.box_rows * pl.box_w * 4;
+    int tma_rows = pl.box_rows;
+    if (const char* e = std::getenv("CB_TS_HACK_ROWS")) tma_rows = std::atoi(e);  // TIMING EXPERIMENT ONLY (wrong results)
+    pl.stage_bytes = (uint32_t)g.C * tma_rows * pl.box_w * 4;
     pl.stage_stride = (pl.stage_bytes + 1023) / 1024 * 1024;
     // CTA pairs halve each SM's weight reads (the B operand, ~30% of the shared-memory
     // traffic of a tile): N split N/2 per CTA, needs N/2 a multiple of 16 (SW128 atoms)
@@ -765,7 +884,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
         cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.C, (cuuint64_t)g.N};
         cuuint64_t strides[3] = {(cuuint64_t)g.W * 4, (cuuint64_t)g.HW * 4,
                                  (cuuint64_t)g.C * g.HW * 4};
-        cuuint32_t box[4] = {(cuuint32_t)pl.box_w, (cuuint32_t)pl.box_rows, (cuuint32_t)g.C, 1};
+        cuuint32_t box[4] = {(cuuint32_t)pl.box_w, (cuuint32_t)(pl.stage_bytes / (4u * g.C * pl.box_w)), (cuuint32_t)g.C, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -823,7 +942,8 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.w_rows = pl.n_pad / pl.cg;
     if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
     if (std::getenv("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
-    const TsKernel kern = pl.cg == 2 ? ts_kernel_for<2>(prm.fixed, pl.pair) : ts_kernel_for<1>(prm.fixed, pl.pair);
+    const int mode = pl.pair == 2 ? 2 + pl.pf : pl.pair;
+    const TsKernel kern = pl.cg == 2 ? ts_kernel_for<2>(prm.fixed, mode) : ts_kernel_for<1>(prm.fixed, mode);
     {
         static std::mutex mu;
         static std::set<const void*> ready;  // kernels whose smem attribute is set

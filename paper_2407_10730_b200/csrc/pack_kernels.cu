@@ -412,14 +412,17 @@ int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float
 
 // K3 for K7's pair layout: rows K x kdim_pad, k = (c*R + r)*(S+1) + s', the pad tap s' = 0
 // (pf = 1) or s' = S (pf = 0) zero, split into bf16 (hi, lo).
-__global__ void weight_split_pairs_kernel(int K, int C, int R, int S, int pf, int kdim_pad,
+__global__ void weight_split_pairs_kernel(int K, int C, int R, int S, int pf, int kdim_pad, int mixed,
                                           const float* __restrict__ w, uint16_t* __restrict__ hi_out,
                                           uint16_t* __restrict__ lo_out) {
     const int f = blockIdx.y;
     const int SP = S + 1, KD = C * R * SP;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kdim_pad; k += gridDim.x * blockDim.x) {
         float v = 0.f;
-        if (k < KD) {
+        if (mixed) {  // the K7 mixed layout (cb_common.cuh: mixed_map)
+            const MixedTap t = mixed_map(k, C * R, S, pf);
+            if (t.cr >= 0) v = w[((int64_t)f * C + t.cr / R) * R * S + (t.cr % R) * S + t.s];
+        } else if (k < KD) {
             const int cr = k / SP, s = k - cr * SP - pf;
             if (s >= 0 && s < S) v = w[((int64_t)f * C + cr / R) * R * S + (cr % R) * S + s];
         }
@@ -429,12 +432,12 @@ __global__ void weight_split_pairs_kernel(int K, int C, int R, int S, int pf, in
     }
 }
 
-int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, const float* w, void* hi, void* lo,
-                              cudaStream_t st) {
+int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, int mixed, const float* w, void* hi,
+                              void* lo, cudaStream_t st) {
     if (g.K == 0) return CB_OK;
     if (g.K > 65535) return fail(CB_ERR_UNSUPPORTED, "too many output channels for weight pack");
     const dim3 grid((unsigned)((kdim_pad + 255) / 256), (unsigned)g.K);
-    weight_split_pairs_kernel<<<grid, 256, 0, st>>>(g.K, g.C, g.R, g.S, pf, kdim_pad, w,
+    weight_split_pairs_kernel<<<grid, 256, 0, st>>>(g.K, g.C, g.R, g.S, pf, kdim_pad, mixed, w,
                                                     static_cast<uint16_t*>(hi), static_cast<uint16_t*>(lo));
     return check_launch("weight_split_pairs");
 }
