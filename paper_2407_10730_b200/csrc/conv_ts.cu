@@ -5,16 +5,18 @@
 // trips a re-laid-out copy of the input through HBM; with N = 64 output channels its
 // shared-memory-operand MMAs are bound by the A-operand reads.  Here instead:
 //
-//   * warp 12 (TMA) stages the zero-padded fp32 input rows one 128-pixel tile needs
+//   * the TMA warp stages the zero-padded fp32 input rows one 128-pixel tile needs
 //     ([C][rows][W + 2*pw] box of the NCHW tensor, out-of-range rows/cols zero-filled by
-//     the TMA unit) into a double-buffered smem window, and loads the split weights once;
-//   * warps 0-7 (producers, two per TMEM lane quadrant, each half of the K chunks) build
-//     the tile's A operand -- pixel row m, reduction k = (c, r, s) in OIHW order -- from
+//     the TMA unit) into a ring of smem windows, and loads the split weights once;
+//   * the producer warps (CB_TS_KPARTS per TMEM lane quadrant, default one: the kernel is
+//     bound by shared-memory bandwidth, more producers only add per-tile overhead) build
+//     the tile's A operand -- pixel row m, reduction k in the plan's layout (OIHW order,
+//     padded tap pairs, or the mixed pairs + singles layout of cb_common.cuh) -- from
 //     the window, split every value into bf16 (hi, lo) and write both halves straight into
 //     TMEM with tcgen05.st (no smem A tile, no activation pre-pass, no workspace);
-//   * warp 13 issues, per 16-wide K step, A_lo*B_hi, A_hi*B_lo, A_hi*B_hi as
+//   * the MMA warp issues, per 16-wide K step, A_lo*B_hi, A_hi*B_lo, A_hi*B_hi as
 //     tcgen05.mma kind::f16 with A read from TMEM and B (weights, K-major SW128) from smem;
-//   * warps 8-11 (epilogue) drain the double-buffered TMEM accumulator into NCHW (+bias).
+//   * four epilogue warps drain the double-buffered TMEM accumulator into NCHW (+bias).
 //
 // Tiles are 128 consecutive output pixels of one image; the persistent grid walks them.
 // HBM traffic is the algorithmic minimum: x read once (the window re-reads hit L2), y
@@ -410,6 +412,9 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     else
         __syncthreads();
     ptx::tc_fence_after();
+    // everything above (barriers, TMEM, descriptor prefetch) touches no global memory: with
+    // a programmatic launch it overlaps the stream predecessor's tail
+    ptx::grid_dependency_wait();
     // the leader's barriers, addressed from either CTA of a pair
     const uint32_t a_full_l0 = CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&a_full[0]), 0) : 0;
     const uint32_t acc_empty_l0 = CG == 2 ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), 0) : 0;
@@ -615,7 +620,8 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 }
             }
         }
-        if (issuer) ptx::bulk_wait_all();
+        // the staging buffers must outlive the stores' reads; the kernel boundary completes the writes
+        if (issuer) ptx::bulk_wait_read<0>();
     } else if (warp == TS_TMA_WARP) {
         // ============================ TMA: weights once, then input windows =============
         const uint32_t leader = ptx::elect_one();
@@ -795,9 +801,7 @@ static TsPlan plan_ts(const Geom& g) {
     const int out_rows = std::min(g.P, (TS_BM - 1) / std::max(1, g.Q) + 2);
     pl.box_rows = (out_rows - 1) * g.sh + (g.R - 1) * g.dh + 1;
     if (pl.box_w > 256 || pl.box_rows > 256 || g.C > 256 || (g.W % 4) != 0) return pl;
-    int tma_rows = pl.box_rows;
-    if (const char* e = std::getenv("CB_TS_HACK_ROWS")) tma_rows = std::atoi(e);  // TIMING EXPERIMENT ONLY (wrong results)
-    pl.stage_bytes = (uint32_t)g.C * tma_rows * pl.box_w * 4;
+    pl.stage_bytes = (uint32_t)g.C * pl.box_rows * pl.box_w * 4;
     pl.stage_stride = (pl.stage_bytes + 1023) / 1024 * 1024;
     // CTA pairs halve each SM's weight reads (the B operand, ~30% of the shared-memory
     // traffic of a tile): N split N/2 per CTA, needs N/2 a multiple of 16 (SW128 atoms)
@@ -884,7 +888,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
         cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.C, (cuuint64_t)g.N};
         cuuint64_t strides[3] = {(cuuint64_t)g.W * 4, (cuuint64_t)g.HW * 4,
                                  (cuuint64_t)g.C * g.HW * 4};
-        cuuint32_t box[4] = {(cuuint32_t)pl.box_w, (cuuint32_t)(pl.stage_bytes / (4u * g.C * pl.box_w)), (cuuint32_t)g.C, 1};
+        cuuint32_t box[4] = {(cuuint32_t)pl.box_w, (cuuint32_t)pl.box_rows, (cuuint32_t)g.C, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -961,13 +965,23 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     cfg.blockDim = dim3(TS_THREADS);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = pl.cg;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int nattr = 0;
+    static const bool pdl = std::getenv("CB_NO_PDL") == nullptr;
+    if (pdl) {  // the prologue may overlap the stream predecessor (grid_dependency_wait)
+        attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[nattr].val.programmaticStreamSerializationAllowed = 1;
+        ++nattr;
+    }
+    if (pl.cg == 2) {  // no cluster attribute for single CTAs
+        attr[nattr].id = cudaLaunchAttributeClusterDimension;
+        attr[nattr].val.clusterDim.x = pl.cg;
+        attr[nattr].val.clusterDim.y = 1;
+        attr[nattr].val.clusterDim.z = 1;
+        ++nattr;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pl.cg == 2 ? 1 : 0;  // no cluster attribute for single CTAs
+    cfg.numAttrs = nattr;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mx, mwh, mwl, my);
     if (e != cudaSuccess) return fail(CB_ERR_CUDA, std::string("conv_ts launch: ") + cudaGetErrorString(e));
     return check_launch("conv_ts_kernel");

@@ -137,6 +137,12 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
+// Programmatic dependent launch: a kernel launched with the programmatic-stream-serialization
+// attribute may start while its stream predecessor is still draining; it must not touch
+// global memory the predecessor writes before this wait (which also makes those writes
+// visible).  Without the attribute the wait returns at once.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // im2col-mode TMA over an NHWC tensor: loads `pixelsPerColumn` pixels starting at input
