@@ -419,28 +419,12 @@ def config_table(peaks, runs: int = 5):
         flush_rd.sum()
     hbm = peaks["hbm_gbs"] * 1e9
 
-    def kernel_alone_us(d, variant, inp, reps: int = 10, replays: int = 5) -> float:
-        """The fused conv kernel alone (weights packed, K0 done), L2 flushed before every
-        launch, without event nodes around it: median replay of a graph of reps x (flush,
-        kernel) minus the same graph without the kernel.  An event-bracketed phase also
-        holds the event nodes' own few microseconds, which dominate the small configs."""
-        import ctypes
-        from paper_2407_10730_b200 import _capi
-        lib, cd, vid = _capi.load(), _capi.cdesc(d), _capi.variant_id(variant)
-        hi, lo, wf = algos.pack_fused_weights(inp.weights, d, variant)
-        ws = algos.fused_workspace(d, variant)
-        nbytes = ws.numel() if ws is not None else 0
-        wsp = ws.data_ptr() if ws is not None else None
-        y = torch.empty((d.batch, d.out_channels) + algos.output_shape(d), device="cuda")
-        ptr = lambda t: None if t is None else t.data_ptr()
-        cur = lambda: torch.cuda.current_stream().cuda_stream
-        if variant != "ffma":
-            _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), inp.input.data_ptr(), wsp, nbytes, cur()))
-
-        def kern():
-            _capi.check(lib.cb_conv_fused_packed(vid, ctypes.byref(cd), inp.input.data_ptr(), wsp, nbytes,
-                                                 ptr(hi), ptr(lo), ptr(wf), None, y.data_ptr(), cur()))
-        kern()
+    def alone_us(launch, reps: int = 10, replays: int = 5) -> float:
+        """One kernel alone, L2 flushed before every launch, without event nodes around it:
+        median replay of a graph of reps x (flush, launch) minus the same graph without the
+        launch.  An event-bracketed phase also holds the event nodes' own few microseconds,
+        which dominate the small configs."""
+        launch()
         torch.cuda.synchronize()
         med = []
         for with_k in (True, False):
@@ -449,7 +433,7 @@ def config_table(peaks, runs: int = 5):
                 for _ in range(reps):
                     flush_l2()
                     if with_k:
-                        kern()
+                        launch()
             g.replay()
             torch.cuda.synchronize()
             ts = []
@@ -463,6 +447,40 @@ def config_table(peaks, runs: int = 5):
             med.append(sorted(ts)[len(ts) // 2])
             del g
         return med[0] - med[1]
+
+    import ctypes
+    from paper_2407_10730_b200 import _capi
+    lib = _capi.load()
+    cur = lambda: torch.cuda.current_stream().cuda_stream
+    ptr = lambda t: None if t is None else t.data_ptr()
+
+    def kernel_alone_us(d, variant, inp) -> float:
+        """The fused conv kernel alone (weights packed, K0 done) through the C ABI."""
+        cd, vid = _capi.cdesc(d), _capi.variant_id(variant)
+        hi, lo, wf = algos.pack_fused_weights(inp.weights, d, variant)
+        ws = algos.fused_workspace(d, variant)
+        nbytes = ws.numel() if ws is not None else 0
+        wsp = ws.data_ptr() if ws is not None else None
+        y = torch.empty((d.batch, d.out_channels) + algos.output_shape(d), device="cuda")
+        if variant != "ffma":
+            _capi.check(lib.cb_fused_pack_input(vid, ctypes.byref(cd), inp.input.data_ptr(), wsp, nbytes, cur()))
+        return alone_us(lambda: _capi.check(lib.cb_conv_fused_packed(
+            vid, ctypes.byref(cd), inp.input.data_ptr(), wsp, nbytes, ptr(hi), ptr(lo), ptr(wf), None,
+            y.data_ptr(), cur())))
+
+    def pack_alone_us(d, inp, slices: bool) -> float:
+        """K1 (the im2col matrix) or K2 (every SConv slice in one launch) alone."""
+        cd = _capi.cdesc(d)
+        oh, ow = algos.output_shape(d)
+        cols = torch.empty(d.in_channels // d.groups * d.k_h * d.k_w * d.groups * d.batch * oh * ow,
+                           device="cuda")
+        if not slices:
+            return alone_us(lambda: _capi.check(lib.cb_im2col_f32(
+                ctypes.byref(cd), inp.input.data_ptr(), cols.data_ptr(), cur())))
+        sp = _capi.CbSlicePlan()
+        _capi.check(lib.cb_sconv_plan(ctypes.byref(cd), oh * ow, ctypes.byref(sp)))
+        return alone_us(lambda: _capi.check(lib.cb_sconv_pack_f32(
+            ctypes.byref(cd), ctypes.byref(sp), 0, sp.num_slices, inp.input.data_ptr(), cols.data_ptr(), cur())))
     table, samples = {}, {}
     for name in TABLE_CONFIGS:
         d = CONFIGS[name]
@@ -524,6 +542,11 @@ def config_table(peaks, runs: int = 5):
                 ent["pack_gbs"] = rl["pack_bytes"] / (pk * 1e-9) / 1e9 if pk else None
                 ent["pack_hbm_frac"] = rl["pack_bytes"] / (pk * 1e-9) / hbm if pk else None
                 ent["target_70pct_met"] = bool(pk and rl["pack_bytes"] / (pk * 1e-9) / hbm >= 0.7)
+                if not tag.endswith("_tf32"):  # the pack kernels do not depend on the split
+                    pa = pack_alone_us(d, inp, slices=not im2)
+                    ent["pack_alone_us"] = pa
+                    ent["pack_alone_hbm_frac"] = rl["pack_bytes"] / (pa * 1e-6) / hbm if pa > 0 else None
+                    ent["target_70pct_met"] = bool(pa > 0 and rl["pack_bytes"] / (pa * 1e-6) / hbm >= 0.7)
                 pack = st.phase_ns_mean[Phase.IN_PACKING] + (
                     st.phase_ns_mean[Phase.PRE_REORDER] if im2 else 0.0)
                 ent["pack_share"] = pack / op if op else None

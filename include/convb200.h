@@ -183,6 +183,14 @@ typedef struct cb_fused_layout {
 
 int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* layout);
 
+/* Reduction layout of the direct few-channel path (path 2, K7): the packed weight rows and
+ * the kernel's A operand order the reduction as map[k] = (c * k_h + r) * k_w + s, the OIHW
+ * offset of the tap at position k, or -1 for a zero element (pad taps).  Writes min(*kdim,
+ * capacity) entries; *kdim is the layout's length before rounding to weight_cols.
+ * CB_ERR_UNSUPPORTED for the other paths.  Host arithmetic only. */
+int cb_fused_reduction_map(int variant, const cb_conv_desc* d, int32_t capacity, int32_t* map,
+                           int32_t* kdim);
+
 /* Tile plan of cb_conv_fused_packed (the persistent grid for path 1). */
 int cb_fused_plan_tiles(int variant, const cb_conv_desc* d, cb_tile_plan* plan);
 

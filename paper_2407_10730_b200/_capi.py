@@ -32,7 +32,8 @@ EXPORTS = (
     "cb_workspace_bytes", "cb_im2col_f32", "cb_sconv_plan", "cb_sconv_range",
     "cb_sconv_pack_f32", "cb_plan_tiles",
     "cb_split_kdim", "cb_weight_split", "cb_gemm", "cb_conv_gemm_cols", "cb_sconv_gemm",
-    "cb_unpack_f32", "cb_fused_layout_query", "cb_fused_plan_tiles", "cb_fused_pack_weights",
+    "cb_unpack_f32", "cb_fused_layout_query", "cb_fused_reduction_map", "cb_fused_plan_tiles",
+    "cb_fused_pack_weights",
     "cb_fused_pack_input", "cb_conv_fused_packed", "cb_conv_fused",
 )
 
@@ -106,6 +107,8 @@ _SIGNATURES = {
                       ctypes.c_int),
     "cb_unpack_f32": ([_DESC, _PLAN, _I32, _I32, _P, _P, _P, _P], ctypes.c_int),
     "cb_fused_layout_query": ([ctypes.c_int, _DESC, ctypes.POINTER(CbFusedLayout)], ctypes.c_int),
+    "cb_fused_reduction_map": ([ctypes.c_int, _DESC, _I32, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
     "cb_fused_plan_tiles": ([ctypes.c_int, _DESC, ctypes.POINTER(CbTilePlan)], ctypes.c_int),
     "cb_fused_pack_weights": ([ctypes.c_int, _DESC, _P, _P, _P, _P], ctypes.c_int),
     "cb_fused_pack_input": ([ctypes.c_int, _DESC, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),

@@ -622,6 +622,18 @@ def fused_layout(desc, variant: str = FUSED_AUTO) -> dict:
                                      variant, _env_key()))
 
 
+def fused_reduction_map(desc, variant: str = "tc3xbf16") -> list:
+    """cb_fused_reduction_map: the reduction order of the direct few-channel path (K7) --
+    entry k is the OIHW offset (c * k_h + r) * k_w + s of the tap at position k, or -1 for a
+    zero element.  Raises UnsupportedDescriptorError for descriptors the other paths serve."""
+    cap = 4096
+    buf = (ctypes.c_int32 * cap)()
+    kd = ctypes.c_int32()
+    _capi.check(_capi.load().cb_fused_reduction_map(_capi.variant_id(variant), ctypes.byref(_cd(desc)),
+                                                    cap, buf, ctypes.byref(kd)))
+    return list(buf[:min(kd.value, cap)])
+
+
 def fused_plan(desc, variant: str = FUSED_AUTO) -> dict:
     """cb_fused_plan_tiles: the tile plan of the fused kernel for this descriptor."""
     variant = resolve_variant(desc, variant)

@@ -131,6 +131,7 @@ int tma_tail_counters(const Geom& g, const FusedLayout& L);
 int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
                    const float* bias, float* y, cudaStream_t st);
 int ts_plan_query(const Geom& g, cb_tile_plan* out);
+int ts_reduction_map(const Geom& g, int cap, int32_t* map);
 int ts_weight_kdim(const Geom& g, int* pair, int* pf);
 int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, int mixed, const float* w, void* hi,
                               void* lo, cudaStream_t st);
@@ -514,6 +515,21 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
     out->weight_cols = L.tma ? L.kw_pad
                              : cb_split_kdim(L.ts ? ts_weight_kdim(g, &ts_pair, &ts_pf) : g.kdim);  // K7 / K4
     out->workspace_bytes = act_ws_bytes(gk, L);
+    return CB_OK;
+}
+
+int cb_fused_reduction_map(int variant, const cb_conv_desc* d, int32_t capacity, int32_t* map,
+                           int32_t* kdim) {
+    Geom g, gk;
+    FusedLayout L;
+    int rc = fused_setup(variant, d, &g, &L, &gk);
+    if (rc) return rc;
+    if (!kdim || (capacity > 0 && !map)) return fail(CB_ERR_INVALID, "null out pointer");
+    if (variant == CB_VARIANT_FFMA || !L.ts)
+        return fail(CB_ERR_UNSUPPORTED, "only the direct few-channel path (path 2) has a reduction map");
+    const int kd = ts_reduction_map(g, capacity, map);
+    if (kd < 0) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
+    *kdim = kd;
     return CB_OK;
 }
 

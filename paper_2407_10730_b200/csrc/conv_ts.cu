@@ -842,6 +842,29 @@ int ts_weight_kdim(const Geom& g, int* pair, int* pf) {
     return pl.pair ? pl.kdim : g.kdim;
 }
 
+// The K7 reduction layout, element by element: map[k] = the OIHW index (c*R + r)*S + s of the
+// weight / window tap at reduction position k, or -1 for a zero element (pad taps, the tail).
+// Returns the layout's length (ts_weight_kdim), or -1 when K7 does not serve the descriptor.
+int ts_reduction_map(const Geom& g, int cap, int32_t* map) {
+    const TsPlan pl = plan_ts(g);
+    if (!pl.ok) return -1;
+    const int kd = pl.pair ? pl.kdim : g.kdim;
+    for (int k = 0; k < kd && k < cap; ++k) {
+        int v = -1;
+        if (pl.pair == 2) {
+            const MixedTap t = mixed_map(k, g.C * g.R, g.S, pl.pf);
+            if (t.cr >= 0) v = t.cr * g.S + t.s;
+        } else if (pl.pair == 1) {
+            const int cr = k / (g.S + 1), s = k - cr * (g.S + 1) - pl.pf;
+            if (s >= 0 && s < g.S) v = cr * g.S + s;
+        } else {
+            v = k;
+        }
+        map[k] = v;
+    }
+    return kd;
+}
+
 int ts_plan_query(const Geom& g, cb_tile_plan* out) {
     const TsPlan pl = plan_ts(g);
     if (!pl.ok) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");

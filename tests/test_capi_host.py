@@ -188,3 +188,44 @@ def test_fused_tile_plans(lib):
     from paper_2407_10730_b200.descriptor import parse_key
     big = algos.fused_plan(parse_key("n1_c2048x56x56_f256x7x7_s1x1_p3x3_d1x1_g1_b0"), "tc3xbf16")
     assert (big["block_m"], big["m_tiles"], big["ctas"]) == (256, 13, 130), big
+
+
+@pytest.mark.parametrize("key,mixed", [
+    ("n16_c3x224x224_f64x7x7_s2x2_p3x3_d1x1_g1_b0", True),    # cfg3: pairs + singles, no pad taps
+    ("n2_c3x32x32_f16x3x3_s2x2_p1x1_d1x1_g1_b0", True),
+    ("n2_c3x32x32_f16x5x5_s2x2_p2x2_d1x1_g1_b0", True),
+    ("n2_c4x32x32_f32x3x3_s2x2_p1x1_d1x1_g1_b0", True),
+    ("n2_c4x32x32_f32x7x7_s2x2_p3x3_d1x1_g1_b0", True),
+    ("n2_c3x32x32_f16x3x3_s1x1_p1x1_d1x1_g1_b0", False),      # odd stride: plain OIHW order
+    ("n2_c8x32x32_f16x3x3_s2x2_p1x1_d1x1_g1_b0", False),      # no compile-time layout: plain
+])
+def test_k7_reduction_map_is_a_permutation(lib, key, mixed):
+    """cb_fused_reduction_map (host arithmetic): K7's reduction layout covers every (c, r, s)
+    tap exactly once; the mixed layout (even horizontal stride, odd S) has no pad taps inside
+    rows, keeps each aligned tap pair (k even, k + 1) on adjacent window columns of one
+    (c, r) row, and pairs the rows' single taps two rows at a time."""
+    from paper_2407_10730_b200 import algos
+    from paper_2407_10730_b200.descriptor import parse_key
+    d = parse_key(key)
+    assert algos.fused_layout(d, "tc3xbf16")["path"] == 2
+    m = algos.fused_reduction_map(d)
+    crs = d.in_channels * d.k_h * d.k_w
+    taps = [v for v in m if v >= 0]
+    assert sorted(taps) == list(range(crs))
+    if not mixed:
+        assert m == list(range(crs))
+        return
+    S, nr = d.k_w, d.in_channels * d.k_h
+    assert len(m) == crs + (nr & 1)             # one zero element after an odd last row
+    assert all(v >= 0 for v in m[:crs - 1])
+    singles = 0
+    for k in range(0, len(m) - 1, 2):
+        a, b = m[k], m[k + 1]
+        if a >= 0 and b >= 0 and a // S == b // S:
+            assert b == a + 1                   # one LDS.64 of two adjacent columns
+        else:
+            singles += 1                        # two rows' single taps (or single + zero)
+            if b >= 0:
+                assert b // S == a // S + 1 and b % S == a % S
+    assert singles == (nr + 1) // 2
+    assert algos.fused_layout(d, "tc3xbf16")["weight_cols"] == _capi.load().cb_split_kdim(len(m))
