@@ -391,7 +391,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             ptx::mbar_init(&a_full[b], CG * TS_PROD_WARPS);
             ptx::mbar_init(&a_empty[b], 1);
             ptx::mbar_init(&acc_full[b], 1);
-            ptx::mbar_init(&acc_empty[b], CG * 128);
+            ptx::mbar_init(&acc_empty[b], CG * 4);  // one arriving lane per epilogue warp
         }
         ptx::fence_mbar_init();
     }
@@ -581,10 +581,13 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 ptx::tmem_ld_wait();
                 if (c0 + 32 >= g.K) {  // accumulator fully in registers: release it early
                     ptx::tc_fence_before();
-                    if (CG == 2)
-                        ptx::mbar_arrive_remote(acc_empty_l0 + b * sizeof(uint64_t));
-                    else
-                        ptx::mbar_arrive(&acc_empty[b]);
+                    __syncwarp();
+                    if (lane == 0) {  // (128 remote arrivals a tile serialise at the leader's barrier)
+                        if (CG == 2)
+                            ptx::mbar_arrive_remote(acc_empty_l0 + b * sizeof(uint64_t));
+                        else
+                            ptx::mbar_arrive(&acc_empty[b]);
+                    }
                     if (threadIdx.x == TS_EPI_WARP0 * 32) ts_stamp(p, 8, i);
                 }
                 if (p.debug & 8) continue;
