@@ -786,7 +786,7 @@ static TsPlan plan_ts(const Geom& g) {
     // pairs, kept for A/B runs with CB_TS_PAIRMODE=1)
     pl.pair = 0;
     pl.pf = (pl.x0 - g.pw) & 1;
-    static const int pair_mode = [] {
+    const int pair_mode = [] {  // read per call: the tests switch layouts in-process
         const char* e = std::getenv("CB_TS_PAIRMODE");
         return std::getenv("CB_TS_NO_PAIR") ? 0 : e ? std::atoi(e) : 2;
     }();

@@ -329,13 +329,16 @@ K7_SHAPES = [(3, 7, 7), (3, 3, 3), (3, 5, 5), (4, 3, 3), (4, 7, 7), (2, 5, 3), (
 
 @pytest.mark.parametrize("crs", K7_SHAPES)
 @pytest.mark.parametrize("stride", [1, 2])
-@pytest.mark.parametrize("generic", [False, True, "no_pair"])
+@pytest.mark.parametrize("generic", [False, True, "no_pair", "padded_pairs"])
 def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
     from paper_2407_10730_b200.algos import conv_fused, fused_layout
     from paper_2407_10730_b200.descriptor import ConvDescriptor
     c, r, s = crs
-    if generic == "no_pair":  # compile-time producers without the padded pair layout
+    if generic == "no_pair":  # compile-time producers in plain OIHW order (one LDS per tap)
         monkeypatch.setenv("CB_TS_NO_PAIR", "1")
+        generic = False
+    elif generic == "padded_pairs":  # one zero pad tap per row instead of the mixed layout
+        monkeypatch.setenv("CB_TS_PAIRMODE", "1")
         generic = False
     elif generic:
         monkeypatch.setenv("CB_TS_GENERIC", "1")
@@ -348,6 +351,28 @@ def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
         assert fused_layout(d, "tc3xbf16")["path"] == 2, d
         inp, (x, w, b) = _inputs(d)
         _check_conv(d, conv_fused(inp, variant="tc3xbf16"), orc.conv_direct_naive(d, x, w, b))
+
+
+def test_direct_few_channel_conv_is_repeatable(cuda):
+    """K7's pipeline (window ring, TMEM A ring, two accumulators, cross-tile barrier tests)
+    gives bit-identical results launch after launch on a grid with many tiles per CTA."""
+    import torch
+    from paper_2407_10730_b200.algos import conv_fused, fused_layout
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    d = ConvDescriptor(batch=12, in_channels=3, in_h=224, in_w=224, out_channels=64, k_h=7, k_w=7,
+                       stride_h=2, stride_w=2, pad_h=3, pad_w=3)
+    assert fused_layout(d, "tc3xbf16")["path"] == 2
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand((d.batch, 3, 224, 224), device="cuda", generator=g) * 2 - 1
+    w = torch.rand((64, 3, 7, 7), device="cuda", generator=g) * 2 - 1
+    from paper_2407_10730_b200.algos import ConvInputs
+    inp = ConvInputs(desc=d, input=x, weights=w)
+    first = conv_fused(inp, variant="tc3xbf16").clone()
+    for _ in range(40):
+        assert torch.equal(conv_fused(inp, variant="tc3xbf16"), first)
+    ref = torch.nn.functional.conv2d(x[:2].double().cpu(), w.double().cpu(), stride=2, padding=3)
+    err = (first[:2].double().cpu() - ref).abs().max().item() / (3 * 7 * 7) ** 0.5
+    assert err <= 1e-4, err
 
 
 @pytest.mark.parametrize("variant", ["tc3xbf16", "tc3xtf32"])
