@@ -95,6 +95,11 @@ int cb_event_destroy(void* event);
 int cb_event_record(void* event, void* stream, int external);
 int cb_event_elapsed_ns(void* start, void* end, int64_t* ns);
 
+/* Hash of the CB_* diagnostics switches in the process environment (their names and
+ * values): the key host-side callers put on cached layouts and plans, since the switches
+ * change both.  One pass over environ. */
+uint64_t cb_env_fingerprint(void);
+
 /* output_shape (descriptor.py:84-92) with the same validation as ConvDescriptor. */
 int cb_output_shape(const cb_conv_desc* d, int32_t* out_h, int32_t* out_w);
 

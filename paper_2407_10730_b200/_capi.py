@@ -28,7 +28,7 @@ TC_VARIANTS = ("tc3xtf32", "tc3xbf16")
 EXPORTS = (
     "cb_version", "cb_last_error_string", "cb_device_sm_count", "cb_launch_count",
     "cb_event_create", "cb_event_destroy", "cb_event_record", "cb_event_elapsed_ns",
-    "cb_output_shape",
+    "cb_output_shape", "cb_env_fingerprint",
     "cb_workspace_bytes", "cb_im2col_f32", "cb_sconv_plan", "cb_sconv_range",
     "cb_sconv_pack_f32", "cb_plan_tiles",
     "cb_split_kdim", "cb_weight_split", "cb_gemm", "cb_conv_gemm_cols", "cb_sconv_gemm",
@@ -106,6 +106,7 @@ _SIGNATURES = {
     "cb_sconv_gemm": ([ctypes.c_int, _DESC, _PLAN, _I32, _I32, _P, _P, _P, _P, _P, _P],
                       ctypes.c_int),
     "cb_unpack_f32": ([_DESC, _PLAN, _I32, _I32, _P, _P, _P, _P], ctypes.c_int),
+    "cb_env_fingerprint": ([], ctypes.c_uint64),
     "cb_fused_layout_query": ([ctypes.c_int, _DESC, ctypes.POINTER(CbFusedLayout)], ctypes.c_int),
     "cb_fused_reduction_map": ([ctypes.c_int, _DESC, _I32, ctypes.POINTER(ctypes.c_int32),
                                 ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),

@@ -595,15 +595,17 @@ def conv_main_blocked_direct(inputs, ledger, cache: CacheParams | None = None, *
 # ---------------------------------------------------------------------------------------
 # Fused implicit-GEMM convolution (K6 / K7)
 # ---------------------------------------------------------------------------------------
-def _env_key() -> tuple:
-    """Every CB_* diagnostics switch: the C++ layout and planner read several of them
+def _env_key():
+    """The layout and the planner read diagnostics switches from the environment
     (CB_TMA_*, CB_NO_STACK, CB_NO_TS, CB_FORCE_GATHER, CB_NO_FOLD, CB_STACK_KMAX, ...), so a
-    toggled switch must not reuse a layout (and buffer sizes) cached under another."""
-    return tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("CB_")))
+    toggled switch must not reuse a layout (and buffer sizes) cached under another: the key
+    is the library's hash of every CB_* entry (cb_env_fingerprint, one C pass over environ,
+    ~1 us; walking os.environ from Python costs ~70 us for 130 variables)."""
+    return _capi.load().cb_env_fingerprint()
 
 
 @functools.lru_cache(maxsize=1024)
-def _fused_layout_cached(desc, variant: str, env: tuple) -> tuple:
+def _fused_layout_cached(desc, variant: str, env: int) -> tuple:
     fl = _capi.CbFusedLayout()
     _capi.check(_capi.load().cb_fused_layout_query(_capi.variant_id(variant),
                                                    ctypes.byref(_cd(desc)), ctypes.byref(fl)))
@@ -618,8 +620,9 @@ def fused_layout(desc, variant: str = FUSED_AUTO) -> dict:
     if variant not in _capi.TC_VARIANTS:
         raise ValueError(f"fused_layout describes the tensor-core variants {_capi.TC_VARIANTS}, "
                          f"not {variant!r}")
-    return dict(_fused_layout_cached(ConvDescriptor(**{f: getattr(desc, f) for f in _DESC_FIELDS}),
-                                     variant, _env_key()))
+    key = desc if type(desc) is ConvDescriptor else \
+        ConvDescriptor(**{f: getattr(desc, f) for f in _DESC_FIELDS})  # (the reference's own class)
+    return dict(_fused_layout_cached(key, variant, _env_key()))
 
 
 def fused_reduction_map(desc, variant: str = "tc3xbf16") -> list:

@@ -9,6 +9,16 @@
 
 namespace cb {
 
+// Environment switches on launch paths (CB_*): looked up in a per-thread snapshot of the
+// process environment's CB_ entries, taken once per C-ABI call (make_geom and the entry
+// points without a descriptor refresh it), instead of one libc getenv per switch -- a K6
+// launch reads ~17 switches and every getenv walks the whole environment (~0.3 us each in a
+// typical process, half of the call's host time).  Same result as getenv at the time of the
+// refresh, so in-process toggles (the tests) take effect at the next call.
+void env_refresh();
+const char* env(const char* name);
+
+
 // Diagnostics timelines (CB_TMA_TRACE / CB_TS_TRACE / CB_K8_TRACE) exist only in a build with
 // -DCB_TRACE (build(defines=("-DCB_TRACE",)), loaded with CB_LIB_PATH): in the product build
 // every stamp and the conditions around it compile away.

@@ -609,12 +609,12 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
     G8Params prm = prm_in;
     prm.ring = (G8_TMEM_COLS - BN) / Cfg::CHUNK_COLS;
     prm.astages = 4;
-    if (const char* e = std::getenv("CB_K8_ASTAGES"))  // even: each stage stays with one producer group
+    if (const char* e = env("CB_K8_ASTAGES"))  // even: each stage stays with one producer group
         prm.astages = std::max(2, std::min(G8_ASTAGES_MAX, std::atoi(e))) & ~1;
     const int ostage_bytes = 1024 + 8 * G8_OSTAGE_BYTES;  // barriers' KB + epilogue staging
     prm.bstages = std::min(8, (225 * 1024 - ostage_bytes - prm.astages * G8_ASTAGE_BYTES) / Cfg::STAGE_BYTES);
-    if (const char* e = std::getenv("CB_K8_DEBUG")) prm.debug = std::atoi(e);
-    if (const char* e = std::getenv("CB_K8_BSTAGES")) prm.bstages = std::max(2, std::min(prm.bstages, std::atoi(e)));
+    if (const char* e = env("CB_K8_DEBUG")) prm.debug = std::atoi(e);
+    if (const char* e = env("CB_K8_BSTAGES")) prm.bstages = std::max(2, std::min(prm.bstages, std::atoi(e)));
     if (prm.bstages < 2) return fail(CB_ERR_UNSUPPORTED, "K8: shared memory for 2 weight stages");
     if (8 * (2 * prm.bstages + 2 * prm.ring + 4 + 2 * prm.astages) > 1024)
         return fail(CB_ERR_UNSUPPORTED, "K8: barrier block overflow");
@@ -698,7 +698,7 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
         if (r != CUDA_SUCCESS) prm.tma_y = 0;  // per-lane stores
     }
     const int grid = (int)std::min<int64_t>(prm.items, sm_count());
-    if (std::getenv("CB_K8_TRACE")) prm.trace = debug_trace_buffer(1024, st);  // + chunk stamps
+    if (env("CB_K8_TRACE")) prm.trace = debug_trace_buffer(1024, st);  // + chunk stamps
     kern<<<grid, G8_THREADS, std::max<size_t>(smem, 120 * 1024), st>>>(prm, mh, ml, ma, my);
     return check_launch("gemm_ts_kernel");
 }
@@ -707,7 +707,7 @@ static int launch_g8_cfg(const G8Params& prm_in, const void* w_hi, const void* w
 // caller should fall back to K4.
 int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
                    const void* w_lo, const float* bias, float* out, int add_mode, cudaStream_t st) {
-    if (pm.src_mode == SRC_CONV || std::getenv("CB_NO_K8")) return CB_ERR_UNSUPPORTED;
+    if (pm.src_mode == SRC_CONV || env("CB_NO_K8")) return CB_ERR_UNSUPPORTED;
     if (pm.j_count == 0) return CB_OK;
     G8Params prm{};
     prm.g = g;
@@ -723,7 +723,7 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
         prm.range_chunks = std::max(1, (prm.nchunks + nr - 1) / nr);
     }
     int bn = g.kpg <= 64 ? 64 : g.kpg <= 128 ? 128 : 256;
-    if (const char* e = std::getenv("CB_K8_BN")) bn = std::min(bn, std::max(64, std::atoi(e)));  // diagnostics
+    if (const char* e = env("CB_K8_BN")) bn = std::min(bn, std::max(64, std::atoi(e)));  // diagnostics
     prm.m_tiles = (pm.j_count + G8_BM - 1) / G8_BM;
     // (narrower channel tiles for short grids measured slower: A is rebuilt per channel tile)
     prm.n_tiles = (g.kpg + bn - 1) / bn;
@@ -738,7 +738,7 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
         // (3xBF16): the tail's MMAs drop from 31 to 14-21 us, but the parts' ordered
         // read-add-store epilogues (~1.7 TB/s of NCHW stores chip-wide) give it all back:
         // 94-98 us either way, so the channel split stays the default.
-        const char* ks = std::getenv("CB_K8_KSPLIT");
+        const char* ks = env("CB_K8_KSPLIT");
         const int kmax = ks ? std::atoi(ks) : 0;
         const int kparts = (int)std::min<int64_t>(std::min<int64_t>(grid / std::max<int64_t>(tail, 1), kmax),
                                                   prm.nchunks / 4);
@@ -762,11 +762,11 @@ int launch_gemm_ts(bool bf16, const Geom& g, const PixMap& pm, const float* src,
     }
     prm.tma_a = pm.src_mode == SRC_MATRIX && (pm.src_ld % 4) == 0 &&
                 (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pm.j_begin + pm.j_count <= pm.src_ld &&
-                !std::getenv("CB_K8_NO_TMA_A");
+                !env("CB_K8_NO_TMA_A");
     // TMA-store epilogue: NCHW y (the Im2col-GEMM drop-in) or an output matrix (the SConv
     // accumulators, cb_gemm); 16-byte row strides and base
     prm.tma_y = 0;
-    if (!std::getenv("CB_K8_NO_TMA_STORE") && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !add_mode) {
+    if (!env("CB_K8_NO_TMA_STORE") && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !add_mode) {
         if (pm.dst_mode == DST_NCHW && g.PQ % 4 == 0 && pm.j_begin == 0)
             prm.tma_y = 1;
         else if (pm.dst_mode == DST_MATRIX && pm.dst_ld % 4 == 0)

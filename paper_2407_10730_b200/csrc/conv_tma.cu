@@ -808,7 +808,7 @@ static FusedLayout base_layout(const Geom& g, bool bf16) {
 bool ts_eligible(const Geom& g);
 
 static int stack_kmax() {  // largest K for row stacking (CB_STACK_KMAX overrides; diagnostics)
-    const char* e = std::getenv("CB_STACK_KMAX");
+    const char* e = env("CB_STACK_KMAX");
     return e ? std::atoi(e) : 32;
 }
 
@@ -816,7 +816,7 @@ FusedLayout fused_layout(const Geom& g, bool bf16) {
     FusedLayout L = base_layout(g, bf16);
     // Few output channels, many input channels: stack the taps (see stack_geom).  The TMA
     // im2col walk would re-read every input pixel once per tap for a handful of MMA columns.
-    if (g.G == 1 && g.RS > 1 && !std::getenv("CB_NO_STACK")) {
+    if (g.G == 1 && g.RS > 1 && !env("CB_NO_STACK")) {
         int mode = 0;
         if (g.RS * g.K <= 256 && g.C >= 128) mode = 1;                          // all taps
         else if (g.S > 1 && g.S * g.K <= 256 && g.K <= stack_kmax() && g.C >= 64) mode = 2;  // row taps
@@ -830,18 +830,18 @@ FusedLayout fused_layout(const Geom& g, bool bf16) {
     }
     // Few channels (C <= 16): the direct kernel builds A in TMEM from TMA-staged fp32 rows
     // (no activation pre-pass, no padded taps).  bf16 split only.
-    if (bf16 && g.C <= 16 && !std::getenv("CB_NO_TS") && ts_eligible(g)) {
+    if (bf16 && g.C <= 16 && !env("CB_NO_TS") && ts_eligible(g)) {
         FusedLayout T = L;
         T.tma = 0;
         T.fold = 0;
         T.ts = 1;
         return T;
     }
-    if (std::getenv("CB_FORCE_GATHER")) {  // diagnostics: the K4 gather path (no workspace)
+    if (env("CB_FORCE_GATHER")) {  // diagnostics: the K4 gather path (no workspace)
         L.tma = 0;
         return L;
     }
-    if (g.G == 1 && g.S > 1 && g.C * g.S <= 128 && !std::getenv("CB_NO_FOLD")) {
+    if (g.G == 1 && g.S > 1 && g.C * g.S <= 128 && !env("CB_NO_FOLD")) {
         FusedLayout F = base_layout(fold_geom(g), bf16);
         if (F.tma && (!L.tma || F.num_kb < L.num_kb)) {
             F.fold = g.S;
@@ -874,7 +874,7 @@ static int tail_split_parts(int64_t tiles, int units, int num_kb, int bn) {
     int parts = (int)std::min<int64_t>(std::min<int64_t>(units / tail, num_kb / min_kbp),
                                        tiles > units ? MAX_TAIL_OTHERS + 1 : MAX_SHORT_PARTS);
     const double tile_mma = 12.0 * num_kb * (bn / 2.0);  // cycles, as in plan_tma's model
-    if (parts >= 2 && tile_mma * (1.0 - 1.0 / parts) < 4000.0 && !std::getenv("CB_TMA_TAIL_ALWAYS"))
+    if (parts >= 2 && tile_mma * (1.0 - 1.0 / parts) < 4000.0 && !env("CB_TMA_TAIL_ALWAYS"))
         parts = 1;
     if (parts < 2) return 1;
     const int kbp = (num_kb + parts - 1) / parts;
@@ -883,8 +883,8 @@ static int tail_split_parts(int64_t tiles, int units, int num_kb, int bn) {
 
 static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     const int sms = sm_count();
-    const char* force_cg = std::getenv("CB_TMA_CG");
-    const char* force_bn = std::getenv("CB_TMA_BN");
+    const char* force_cg = env("CB_TMA_CG");
+    const char* force_bn = env("CB_TMA_BN");
     TmaPlan best{};
     best.cg = 1;  // always-valid default: 1-CTA, 64-channel tiles
     best.bn = 64;
@@ -924,7 +924,7 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     // Atomic split-K (bias pre-fill launch + add epilogue) only on request: by default a
     // short grid is filled by the deterministic tail split below (one launch, no atomics).
     pl.splits = 1;
-    const char* splitk = std::getenv("CB_TMA_SPLITK");
+    const char* splitk = env("CB_TMA_SPLITK");
     if (splitk && std::atoi(splitk) == 1 && tiles < units && L.num_kb >= 4) {
         int want = (int)((units + tiles - 1) / tiles);
         pl.splits = std::max(1, std::min(want, L.num_kb / 2));
@@ -944,7 +944,7 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     pl.tail_tiles = 0;
     pl.tail_parts = 1;
     pl.tail_kbp = L.num_kb;
-    const char* no_tail = std::getenv("CB_TMA_TAIL");
+    const char* no_tail = env("CB_TMA_TAIL");
     const int64_t tail = tiles % units;
     if (pl.splits == 1 && tail > 0 && !(no_tail && std::atoi(no_tail) == 0)) {
         int parts = tail_split_parts(tiles, units, L.num_kb, pl.bn);
@@ -960,7 +960,7 @@ static TmaPlan plan_tma(const Geom& g, const FusedLayout& L) {
     // One item per cluster at a time: tail parts then all run concurrently (required, an
     // owner spins on its parts).  The grid cap is a diagnostic for untailed plans only.
     pl.grid = (int)std::min<int64_t>(pl.total_items, units) * pl.cg;
-    if (const char* gcap = std::getenv("CB_TMA_GRID"); gcap && pl.tail_tiles == 0)
+    if (const char* gcap = env("CB_TMA_GRID"); gcap && pl.tail_tiles == 0)
         pl.grid = std::max(pl.cg, std::min(pl.grid, std::atoi(gcap) / pl.cg * pl.cg));
     return pl;
 }
@@ -1117,7 +1117,7 @@ static int launch_tma_cfg(const TmaParams& prm, int grid, const void* ahi, const
     // programmatic dependent launch: the prologue (barriers, TMEM, descriptor prefetch)
     // overlaps the tail of the preceding kernel (K0); griddepcontrol.wait guards the inputs
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("CB_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = env("CB_NO_PDL") ? 0 : 1;
     // cluster dimension only for CTA pairs (a 1-CTA cluster launch measured ~12% slower on
     // the stepwise GEMM)
     attr[1].id = cudaLaunchAttributeClusterDimension;
@@ -1174,7 +1174,7 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
     prm.total_tiles = pl.total_tiles;
     prm.full_items = pl.full_items;
     prm.total_items = pl.total_items;
-    prm.tail_last = std::getenv("CB_TMA_TAIL_LAST") ? 1 : 0;
+    prm.tail_last = env("CB_TMA_TAIL_LAST") ? 1 : 0;
     prm.tail_tiles = pl.tail_tiles;
     prm.tail_parts = pl.tail_parts;
     prm.tail_kbp = pl.tail_kbp;
@@ -1185,17 +1185,17 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
         prm.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(tail_ws) + ctr);
     }
     prm.add_mode = 0;
-    if (const char* dbg = std::getenv("CB_TMA_DEBUG")) prm.debug = std::atoi(dbg);
+    if (const char* dbg = env("CB_TMA_DEBUG")) prm.debug = std::atoi(dbg);
     // Optional TMA-store epilogue (CB_TMA_TSTORE) and bulk-copy tail partials
     // (CB_TMA_BULK_PARTS): measured equal or slower than the direct stores on cfg4 and on
     // output-heavy sweep ops (two epilogue barriers per chunk; tiles crossing images fall
     // back to direct stores anyway), so both are off by default.
     prm.tma_store = (g.PQ % 4 == 0) && (g.G == 1 || g.kpg % 32 == 0) &&
-                    (reinterpret_cast<uintptr_t>(y) & 15) == 0 && std::getenv("CB_TMA_TSTORE");
-    prm.bulk_parts = std::getenv("CB_TMA_BULK_PARTS") ? 1 : 0;
+                    (reinterpret_cast<uintptr_t>(y) & 15) == 0 && env("CB_TMA_TSTORE");
+    prm.bulk_parts = env("CB_TMA_BULK_PARTS") ? 1 : 0;
     prm.out_al16 = (reinterpret_cast<uintptr_t>(y) & 15) == 0 ? 1 : 0;
     prm.range_kb = std::max(1, promote_k(bf16) / (128 / L.eb));
-    if (std::getenv("CB_TMA_TRACE")) prm.trace = debug_trace_buffer(pl.grid, st);
+    if (env("CB_TMA_TRACE")) prm.trace = debug_trace_buffer(pl.grid, st);
     if (pl.splits > 1) {
         int rc = launch_fill_bias(g.N, g.K, g.PQ, bias, y, st);
         if (rc) return rc;

@@ -765,7 +765,7 @@ struct TsPlan {
 };
 
 static int ts_fixed_id(const Geom& g) {
-    if (g.dw != 1 || std::getenv("CB_TS_GENERIC")) return 0;
+    if (g.dw != 1 || env("CB_TS_GENERIC")) return 0;
 #define CB_TS_MATCH(id, c, r, s) \
     if (g.C == c && g.R == r && g.S == s) return id;
     CB_TS_FIXED_LIST(CB_TS_MATCH)
@@ -787,8 +787,8 @@ static TsPlan plan_ts(const Geom& g) {
     pl.pair = 0;
     pl.pf = (pl.x0 - g.pw) & 1;
     const int pair_mode = [] {  // read per call: the tests switch layouts in-process
-        const char* e = std::getenv("CB_TS_PAIRMODE");
-        return std::getenv("CB_TS_NO_PAIR") ? 0 : e ? std::atoi(e) : 2;
+        const char* e = env("CB_TS_PAIRMODE");
+        return env("CB_TS_NO_PAIR") ? 0 : e ? std::atoi(e) : 2;
     }();
     const int kd_pair = pair_mode == 2 ? mixed_kdim(g.C * g.R, g.S) : g.C * g.R * (g.S + 1);
     if (pair_mode && ts_fixed_id(g) && g.S % 2 == 1 && g.sw % 2 == 0 &&
@@ -810,7 +810,7 @@ static TsPlan plan_ts(const Geom& g) {
     // traffic of a tile): N split N/2 per CTA, needs N/2 a multiple of 16 (SW128 atoms)
     pl.cg = 1;
     {
-        const char* e = std::getenv("CB_TS_CG");
+        const char* e = env("CB_TS_CG");
         const int want = e ? std::atoi(e) : 1;  // pairs measured slower on cfg3 (30 vs 22 us)
         if (want == 2 && pl.n_pad % 32 == 0 && pl.n_pad <= 256) pl.cg = 2;
     }
@@ -949,7 +949,7 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     }
     TsParams prm{};
     prm.tma_store = pl.tma_store ? 1 : 0;
-    if (std::getenv("CB_TS_NO_TMA_STORE")) prm.tma_store = 0;
+    if (env("CB_TS_NO_TMA_STORE")) prm.tma_store = 0;
     prm.g = g;
     prm.bias = bias;
     prm.out = y;
@@ -970,8 +970,8 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.nwin = pl.nwin;
     prm.w_half_bytes = pl.w_half_bytes;
     prm.w_rows = pl.n_pad / pl.cg;
-    if (const char* dbg = std::getenv("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
-    if (std::getenv("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
+    if (const char* dbg = env("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
+    if (env("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
     const int mode = pl.pair == 2 ? 2 + pl.pf : pl.pair;
     const TsKernel kern = pl.cg == 2 ? ts_kernel_for<2>(prm.fixed, mode) : ts_kernel_for<1>(prm.fixed, mode);
     {

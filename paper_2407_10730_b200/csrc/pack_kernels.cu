@@ -555,7 +555,7 @@ int launch_unpack(const Geom& g, int band_rows, int64_t j_begin, int64_t j_count
     if (total == 0) return CB_OK;
     if (band_rows >= g.P && g.PQ % 4 == 0 && j_begin % g.PQ == 0 && j_count % g.PQ == 0 &&
         ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(y)) & 15) == 0 &&
-        !std::getenv("CB_K5_ROWS")) {
+        !env("CB_K5_ROWS")) {
         const int64_t nvec = total / 4;
         const int64_t blocks = std::min<int64_t>((nvec + 1023) / 1024, (int64_t)sm_count() * 8);
         unpack_images_kernel<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, st>>>(
@@ -910,7 +910,7 @@ int launch_act_split(bool bf16, const Geom& g, int c_alloc, const float* x, void
     }
     const int64_t in_pix = (int64_t)g.N * g.HW;  // input pixels (not the conv's output npix)
     if (bf16 && g.HW % 4 == 0 && c_alloc % 64 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-        !std::getenv("CB_K0_NARROW") && (in_pix + AS_PX - 1) / AS_PX <= 0x7fffffffLL) {
+        !env("CB_K0_NARROW") && (in_pix + AS_PX - 1) / AS_PX <= 0x7fffffffLL) {
         if ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)
             return fail(CB_ERR_MISALIGNED, "activation workspace must be 16-byte aligned");
         const dim3 wgrid((unsigned)((in_pix + AS_PX - 1) / AS_PX), (unsigned)(c_alloc / 64));
