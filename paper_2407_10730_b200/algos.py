@@ -133,11 +133,17 @@ class CacheParams:
 # ---------------------------------------------------------------------------------------
 # device plumbing (torch: memory + streams only)
 # ---------------------------------------------------------------------------------------
+_TORCH = None
+
+
 def _torch():
-    import torch
-    if not torch.cuda.is_available():
-        raise _capi.ConvB200Error("no CUDA device: the B200 path has no CPU fallback")
-    return torch
+    global _TORCH
+    if _TORCH is None:  # checked until a device is seen, then remembered (called several times per op)
+        import torch
+        if not torch.cuda.is_available():
+            raise _capi.ConvB200Error("no CUDA device: the B200 path has no CPU fallback")
+        _TORCH = torch
+    return _TORCH
 
 
 def _stream() -> int:
@@ -177,6 +183,8 @@ def _dev(a):
     asynchronously on the current stream; numpy arrays through the pinned upload stage."""
     torch = _torch()
     if isinstance(a, torch.Tensor):
+        if a.is_cuda and a.dtype is torch.float32 and a.is_contiguous():
+            return a, False  # the common device-resident case: nothing to do
         host = not a.is_cuda
         t = a.to(device="cuda", dtype=torch.float32, non_blocking=True).contiguous()
         return t, host
