@@ -1,8 +1,8 @@
-mkdir -p gpurun_out/r2bi
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/r2bi/bench.json 2> gpurun_out/r2bi/bench.err; echo "bench rc=$?"; tail -3 gpurun_out/r2bi/bench.err
+mkdir -p gpurun_out/bench_table
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_table/bench.json 2> gpurun_out/bench_table/bench.err; echo "bench rc=$?"; tail -3 gpurun_out/bench_table/bench.err
 python - <<'PY'
 import json
-d=json.loads(open('gpurun_out/r2bi/bench.json').read().strip().splitlines()[-1])
+d=json.loads(open('gpurun_out/bench_table/bench.json').read().strip().splitlines()[-1])
 for c,v in d['configs'].items():
     for p,q in v.items():
         if 'kernel_alone_us' in q: print(c,p,q['variant'],'phase',round(q['kernel_us'],1),'alone',round(q['kernel_alone_us'],1),'frac',round(q['kernel_alone_roofline_frac'],3), q['target_60pct_met'])
