@@ -526,6 +526,12 @@ def config_table(peaks, runs: int = 5):
                    "phases_us": m, "calls": {p.name.lower(): st.calls[p] for p in Phase if st.calls[p]},
                    "roofline_us": rl["t_roofline_s"] * 1e6, "bound": rl["bound"],
                    "op_roofline_frac": rl["t_roofline_s"] / (op * 1e-9) if op else None}
+            # the whole op without the phase events (their nodes cost ~5 us per phase, which
+            # dominates the small configs): same L2-cold differential timing as the kernels
+            oa = alone_us(lambda: fn(inp, algos._NULL_LEDGER), reps=6)
+            ent["operation_alone_us"] = oa
+            ent["gflops_alone"] = rl["flops"] / (oa * 1e-6) / 1e9 if oa > 0 else None
+            ent["op_alone_roofline_frac"] = rl["t_roofline_s"] * 1e6 / oa if oa > 0 else None
             if tag.startswith("fused"):
                 k = st.phase_ns_mean[Phase.IN_MICROKERNEL]
                 ent["kernel_us"] = k / 1e3
