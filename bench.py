@@ -626,6 +626,12 @@ def run_ours(args, ranks):
     from paper_2407_10730_b200.roofline import conv_roofline, load_peaks
 
     rank, world, local = ranks.rank, ranks.world, ranks.local
+    if not torch.cuda.is_available() or local >= torch.cuda.device_count():
+        # one rank per GPU, never several ranks on one device: their kernels would time each other
+        raise SystemExit(f"bench.py: rank {rank} (local {local}) of {world} has no GPU of its own "
+                         f"({torch.cuda.device_count() if torch.cuda.is_available() else 0} visible); "
+                         "--gpus N needs N visible B200s (there is no CPU path; --dry-run exercises "
+                         "the launcher without a device)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
