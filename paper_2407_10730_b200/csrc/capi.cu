@@ -151,13 +151,13 @@ int launch_conv_tma(bool bf16, const Geom& g, const FusedLayout& L, const void* 
 int64_t tma_tail_workspace_bytes(const Geom& g, const FusedLayout& L);
 int debug_trace_copy(unsigned long long* host, int max_ctas, int* slots);
 int tma_tail_counters(const Geom& g, const FusedLayout& L);
-int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
+int launch_conv_ts(const Geom& g, bool bf16, const float* x, const void* w_hi, const void* w_lo,
                    const float* bias, float* y, cudaStream_t st);
-int ts_plan_query(const Geom& g, cb_tile_plan* out);
-int ts_reduction_map(const Geom& g, int cap, int32_t* map);
-int ts_weight_kdim(const Geom& g, int* pair, int* pf);
-int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, int mixed, const float* w, void* hi,
-                              void* lo, cudaStream_t st);
+int ts_plan_query(const Geom& g, bool bf16, cb_tile_plan* out);
+int ts_reduction_map(const Geom& g, bool bf16, int cap, int32_t* map);
+int ts_weight_kdim(const Geom& g, bool bf16, int* pair, int* pf);
+int launch_weight_split_pairs(const Geom& g, bool bf16, int pf, int kdim_pad, int mixed, const float* w,
+                              void* hi, void* lo, cudaStream_t st);
 int ffma_plan_query(const Geom& g, int64_t npix, bool allow_split, cb_tile_plan* out);
 int launch_tc(bool bf16, const Geom& g, const PixMap& pm, const float* src, const void* w_hi,
               const void* w_lo, const float* bias, float* out, int add_mode, int zero_kind,
@@ -547,7 +547,7 @@ int cb_fused_layout_query(int variant, const cb_conv_desc* d, cb_fused_layout* o
     out->k_blocks = L.tma ? L.num_kb : (g.kdim + 128 / L.eb - 1) / (128 / L.eb);
     int ts_pair = 0, ts_pf = 0;
     out->weight_cols = L.tma ? L.kw_pad
-                             : cb_split_kdim(L.ts ? ts_weight_kdim(g, &ts_pair, &ts_pf) : g.kdim);  // K7 / K4
+                             : cb_split_kdim(L.ts ? ts_weight_kdim(g, variant == CB_VARIANT_TC3XBF16, &ts_pair, &ts_pf) : g.kdim);  // K7 / K4
     out->workspace_bytes = act_ws_bytes(gk, L);
     return CB_OK;
 }
@@ -561,7 +561,7 @@ int cb_fused_reduction_map(int variant, const cb_conv_desc* d, int32_t capacity,
     if (!kdim || (capacity > 0 && !map)) return fail(CB_ERR_INVALID, "null out pointer");
     if (variant == CB_VARIANT_FFMA || !L.ts)
         return fail(CB_ERR_UNSUPPORTED, "only the direct few-channel path (path 2) has a reduction map");
-    const int kd = ts_reduction_map(g, capacity, map);
+    const int kd = ts_reduction_map(g, variant == CB_VARIANT_TC3XBF16, capacity, map);
     if (kd < 0) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
     *kdim = kd;
     return CB_OK;
@@ -574,7 +574,7 @@ int cb_fused_plan_tiles(int variant, const cb_conv_desc* d, cb_tile_plan* plan) 
     if (rc) return rc;
     if (!plan) return fail(CB_ERR_INVALID, "null out pointer");
     if (variant == CB_VARIANT_FFMA) return ffma_plan_query(g, g.npix, true, plan);
-    if (L.ts) return ts_plan_query(g, plan);
+    if (L.ts) return ts_plan_query(g, variant == CB_VARIANT_TC3XBF16, plan);
     if (L.tma) return tma_plan_query(gk, variant == CB_VARIANT_TC3XBF16, plan);
     return tc_plan_query(g, g.npix, variant == CB_VARIANT_TC3XBF16, true, plan);
 }
@@ -595,8 +595,8 @@ int cb_fused_pack_weights(int variant, const cb_conv_desc* d, const float* w, vo
                                         L.stack == 1 ? g.RS : L.stack == 2 ? g.S : 0, g.K);
     if (L.ts) {  // K7: plain split rows, or the pair layout with one pad tap per (c, r) row
         int pair = 0, pf = 0;
-        const int kd = ts_weight_kdim(g, &pair, &pf);
-        if (pair) return launch_weight_split_pairs(g, pf, cb_split_kdim(kd), pair == 2, w, w_hi, w_lo, (cudaStream_t)stream);
+        const int kd = ts_weight_kdim(g, bf16, &pair, &pf);
+        if (pair) return launch_weight_split_pairs(g, bf16, pf, cb_split_kdim(kd), pair == 2, w, w_hi, w_lo, (cudaStream_t)stream);
     }
     return launch_weight_split(bf16, g.K, g.kdim, cb_split_kdim(g.kdim), w, w_hi, w_lo,
                                (cudaStream_t)stream);
@@ -633,7 +633,7 @@ int cb_conv_fused_packed(int variant, const cb_conv_desc* d, const float* x, con
     if (variant != CB_VARIANT_FFMA && L.ts) {
         if (!x) return fail(CB_ERR_INVALID, "null input");
         if (!w_hi || !w_lo) return fail(CB_ERR_INVALID, "tensor-core variants need packed weights");
-        return launch_conv_ts(g, x, w_hi, w_lo, b, y, (cudaStream_t)stream);
+        return launch_conv_ts(g, variant == CB_VARIANT_TC3XBF16, x, w_hi, w_lo, b, y, (cudaStream_t)stream);
     }
     if (variant != CB_VARIANT_FFMA && L.tma) {
         if (!ws || (int64_t)ws_bytes < act_ws_bytes(gk, L))

@@ -805,7 +805,7 @@ static FusedLayout base_layout(const Geom& g, bool bf16) {
 // (few channels: C=3 pads each tap to a 16-byte chunk, 147 -> 392 for a 7x7 stem; folded
 // it is 7 taps of 21 -> 24 channels, 147 -> 256) -- fewer MMAs and fewer, larger TMA boxes.
 // Weights are repacked to match (weight_split_taps, fold) and K0 writes the folded rows.
-bool ts_eligible(const Geom& g);
+bool ts_eligible(const Geom& g, bool bf16);
 
 static int stack_kmax() {  // largest K for row stacking (CB_STACK_KMAX overrides; diagnostics)
     const char* e = env("CB_STACK_KMAX");
@@ -829,8 +829,9 @@ FusedLayout fused_layout(const Geom& g, bool bf16) {
         }
     }
     // Few channels (C <= 16): the direct kernel builds A in TMEM from TMA-staged fp32 rows
-    // (no activation pre-pass, no padded taps).  bf16 split only.
-    if (bf16 && g.C <= 16 && !env("CB_NO_TS") && ts_eligible(g)) {
+    // (no activation pre-pass, no padded taps).  The tf32 split only for the compile-time
+    // reduction layouts (one A buffer in TMEM instead of two).
+    if (g.C <= 16 && !env("CB_NO_TS") && !(env("CB_NO_TS_TF32") && !bf16) && ts_eligible(g, bf16)) {
         FusedLayout T = L;
         T.tma = 0;
         T.fold = 0;

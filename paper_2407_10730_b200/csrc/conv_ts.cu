@@ -52,7 +52,10 @@ struct TsParams {
     Geom g;
     const float* bias;
     float* out;
-    int kp;             // reduction padded to 32 (A columns per half: kp / 2)
+    int kp;             // reduction padded to 32 (A columns per half: kp / 2 for bf16 pairs,
+                        // kp for tf32 words)
+    int nab;            // A buffers in TMEM: 2, or 1 when only one fits (tf32)
+    int acols;          // TMEM columns of one A buffer (hi + lo halves)
     int n_pad;          // output channels padded to 16 (MMA N)
     int kb_w;           // split weight row length (multiple of 64)
     int tiles_per_img;  // ceil(PQ / (128 * CG)): tiles of one CTA (CG = 1) or pair (CG = 2)
@@ -145,6 +148,29 @@ __device__ __forceinline__ void split_pair(float v0, float v1, uint32_t& hi, uin
     lo = bf16x2_rn(v0 - __uint_as_float(hi << 16), v1 - __uint_as_float(hi & 0xffff0000u));
 }
 
+// One group of 8 reduction elements (4 value pairs) split and written to the A buffer: bf16
+// halves as 4 + 4 packed words (group g at column 4g), tf32 halves as 8 + 8 words (column 8g).
+template <bool BF16>
+__device__ __forceinline__ void split_store_group(const float (&u)[8], uint32_t a_hi, uint32_t a_lo, int g) {
+    if constexpr (BF16) {
+        uint32_t hv[4], lv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_pair(u[2 * e], u[2 * e + 1], hv[e], lv[e]);
+        ptx::tmem_st_32x32b_groups(a_hi + g * 4, hv, 1);
+        ptx::tmem_st_32x32b_groups(a_lo + g * 4, lv, 1);
+    } else {
+        uint32_t hv[8], lv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const Split2 sp = split_tf32(u[e]);
+            hv[e] = __float_as_uint(sp.hi);
+            lv[e] = __float_as_uint(sp.lo);
+        }
+        ptx::tmem_st_32x32b_groups(a_hi + g * 8, hv, 2);
+        ptx::tmem_st_32x32b_groups(a_lo + g * 8, lv, 2);
+    }
+}
+
 // A producer with the reduction layout fixed at compile time (C, R, S, unit horizontal
 // dilation): groups [G0, G1) of 8 reduction elements k = (c, r, s), each element one LDS at
 // xs + c * cstride + r * rstride + 4 s (the (c, r) row offsets are loop-invariant, the tap an
@@ -174,7 +200,7 @@ __device__ __forceinline__ void load_pair(int k, uint32_t xs, uint32_t xa, uint3
 // Groups [G0, G1) of 8 elements, software-pipelined: the loads of group g + D are issued
 // before group g is split and stored (the volatile LDS / tcgen05.st asm statements keep
 // their source order, so without this every group would wait out a full LDS latency).
-template <int C, int R, int S, int G0, int G1>
+template <int C, int R, int S, int G0, int G1, bool BF16 = true>
 __device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint32_t rstride,
                                             uint32_t a_hi, uint32_t a_lo, bool swap) {
     constexpr int NG = G1 - G0, D = CB_TS_DEPTH;
@@ -195,6 +221,10 @@ __device__ __forceinline__ void build_fixed(uint32_t xs, uint32_t cstride, uint3
         if (step >= D) {
             const int gi = step - D;
             const float* u = v[gi % (D + 1)];
+            if constexpr (!BF16) {
+                split_store_group<false>(v[gi % (D + 1)], a_hi, a_lo, G0 + gi);
+                continue;
+            }
             const int slot = gi % W;
 #pragma unroll
             for (int e = 0; e < 4; ++e) split_pair(u[2 * e], u[2 * e + 1], hv[slot * 4 + e], lv[slot * 4 + e]);
@@ -248,7 +278,7 @@ __device__ __forceinline__ void build_pairs(uint32_t xs_pair, uint32_t cstride, 
 
 // Mixed-layout producer (cb_common.cuh: mixed_map): groups [G0, G1) of 8 elements; a k pair
 // inside a row's pair region is one LDS.64, the pair of two rows' single taps two LDS.32.
-template <int C, int R, int S, int PF, int G0, int G1>
+template <int C, int R, int S, int PF, int G0, int G1, bool BF16 = true>
 __device__ __forceinline__ void build_mixed(uint32_t xs, uint32_t cstride, uint32_t rstride,
                                             uint32_t a_hi, uint32_t a_lo) {
     constexpr int NR = C * R, NG = G1 - G0, D = CB_TS_DEPTH;
@@ -274,6 +304,12 @@ __device__ __forceinline__ void build_mixed(uint32_t xs, uint32_t cstride, uint3
         }
         if (step >= D) {
             const int gi = step - D;
+            if constexpr (!BF16) {
+                const float2* q = v[gi % (D + 1)];
+                const float u[8] = {q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x, q[3].y};
+                split_store_group<false>(u, a_hi, a_lo, G0 + gi);
+                continue;
+            }
             const int slot = gi % W;
 #pragma unroll
             for (int e = 0; e < 4; ++e)
@@ -286,18 +322,18 @@ __device__ __forceinline__ void build_mixed(uint32_t xs, uint32_t cstride, uint3
     }
 }
 
-template <int C, int R, int S, int PF>
+template <int C, int R, int S, int PF, bool BF16 = true>
 __device__ __forceinline__ void build_mixed_part(int kpart, uint32_t xs, uint32_t cstride,
                                                  uint32_t rstride, uint32_t a_hi, uint32_t a_lo) {
     constexpr int G = (mixed_kdim(C * R, S) + 7) / 8, P = CB_TS_KPARTS;
     if (kpart == 0)
-        build_mixed<C, R, S, PF, 0, G * 1 / P>(xs, cstride, rstride, a_hi, a_lo);
+        build_mixed<C, R, S, PF, 0, G * 1 / P, BF16>(xs, cstride, rstride, a_hi, a_lo);
     else if (kpart == 1 && P > 1)
-        build_mixed<C, R, S, PF, G * 1 / P, G * 2 / P>(xs, cstride, rstride, a_hi, a_lo);
+        build_mixed<C, R, S, PF, G * 1 / P, G * 2 / P, BF16>(xs, cstride, rstride, a_hi, a_lo);
     else if (kpart == 2 && P > 2)
-        build_mixed<C, R, S, PF, G * 2 / P, G * 3 / P>(xs, cstride, rstride, a_hi, a_lo);
+        build_mixed<C, R, S, PF, G * 2 / P, G * 3 / P, BF16>(xs, cstride, rstride, a_hi, a_lo);
     else if (P > 3)
-        build_mixed<C, R, S, PF, G * 3 / P, G>(xs, cstride, rstride, a_hi, a_lo);
+        build_mixed<C, R, S, PF, G * 3 / P, G, BF16>(xs, cstride, rstride, a_hi, a_lo);
 }
 
 template <int C, int R, int S>
@@ -315,19 +351,19 @@ __device__ __forceinline__ void build_pairs_part(int kpart, uint32_t xs_pair, ui
 }
 
 // the producer warps of a lane quadrant take contiguous shares of the 8-element groups
-template <int C, int R, int S>
+template <int C, int R, int S, bool BF16 = true>
 __device__ __forceinline__ void build_fixed_part(int kpart, uint32_t xs, uint32_t cstride,
                                                  uint32_t rstride, uint32_t a_hi, uint32_t a_lo,
                                                  bool swap) {
     constexpr int G = (C * R * S + 7) / 8, P = CB_TS_KPARTS;
     if (kpart == 0)
-        build_fixed<C, R, S, 0, G * 1 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
+        build_fixed<C, R, S, 0, G * 1 / P, BF16>(xs, cstride, rstride, a_hi, a_lo, swap);
     else if (kpart == 1 && P > 1)
-        build_fixed<C, R, S, G * 1 / P, G * 2 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
+        build_fixed<C, R, S, G * 1 / P, G * 2 / P, BF16>(xs, cstride, rstride, a_hi, a_lo, swap);
     else if (kpart == 2 && P > 2)
-        build_fixed<C, R, S, G * 2 / P, G * 3 / P>(xs, cstride, rstride, a_hi, a_lo, swap);
+        build_fixed<C, R, S, G * 2 / P, G * 3 / P, BF16>(xs, cstride, rstride, a_hi, a_lo, swap);
     else if (P > 3)
-        build_fixed<C, R, S, G * 3 / P, G>(xs, cstride, rstride, a_hi, a_lo, swap);
+        build_fixed<C, R, S, G * 3 / P, G, BF16>(xs, cstride, rstride, a_hi, a_lo, swap);
 }
 
 // compile-time reduction layouts (TsParams::fixed): 0 = generic offset-table producer
@@ -347,7 +383,10 @@ CB_TS_FIXED_LIST(CB_TS_LAYOUT)
 // One instantiation per (CTA group, compile-time layout FX, pair mode): each kernel holds
 // only its own unrolled producer -- with all layouts in one kernel the ncu profile showed
 // 12% of warp stalls as no_instructions (instruction-cache misses).
-template <int CG, int FX, int MODE>  // MODE: 0 plain, 1 padded pairs, 2 / 3 mixed layout with pf = 0 / 1
+// MODE: 0 plain, 1 padded pairs, 2 / 3 mixed layout with pf = 0 / 1.  BF16 = false: the 3xTF32
+// split (tf32 words in TMEM, kind::tf32 MMAs of 8 reduction elements; compile-time layouts,
+// single CTAs, MODE 0 / 2 / 3 only).
+template <int CG, int FX, int MODE, bool BF16 = true>
 __global__ void __launch_bounds__(TS_THREADS, 1)
 conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUtensorMap tm_x,
                const __grid_constant__ CUtensorMap tm_whi, const __grid_constant__ CUtensorMap tm_wlo,
@@ -379,7 +418,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
     const int unit0 = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;
     const int col_a0 = 2 * p.n_pad;  // TMEM: [acc0 | acc1 | A0 (hi, lo) | A1 (hi, lo)]
-    const int half_cols = p.kp / 2;
+    const int half_cols = BF16 ? p.kp / 2 : p.kp;
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(w_full, 1);
@@ -473,15 +512,15 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             ptx::tc_fence_after();
         }
         while (have) {
-            const int b = i & 1;
+            const int b = p.nab == 2 ? (i & 1) : 0;  // A buffer of tile i
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 2 : 12, i);
-            const uint32_t a_hi = lane_addr + col_a0 + b * p.kp;
+            const uint32_t a_hi = lane_addr + col_a0 + b * p.acols;
             const uint32_t a_lo = a_hi + half_cols;
             if (FX != 0 && !(p.debug & 16)) {
-                if (i < 2) {  // columns past the written groups: zero once per A buffer
+                if (i < p.nab) {  // columns past the written groups: zero once per A buffer
                     const uint32_t z[4] = {0u, 0u, 0u, 0u};
                     const int kd = MODE == 1 ? g.C * g.R * (g.S + 1) : MODE >= 2 ? mixed_kdim(g.C * g.R, g.S) : g.kdim;
-                    for (int c4 = ((kd + 7) / 8) * 4 + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
+                    for (int c4 = ((kd + 7) / 8) * (BF16 ? 4 : 8) + kpart * 4; c4 < half_cols; c4 += 4 * KPARTS) {
                         ptx::tmem_st_32x32b_x4(a_hi + c4, z);
                         ptx::tmem_st_32x32b_x4(a_lo + c4, z);
                     }
@@ -489,12 +528,12 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 const uint32_t cstride = 4u * p.box_rows * p.box_w, rstride = 4u * g.dh * p.box_w;
                 using L = TsLayout<FX>;
                 if constexpr (FX != 0 && MODE >= 2 && L::S % 2 == 1) {
-                    build_mixed_part<L::C, L::R, L::S, MODE - 2>(kpart, xs, cstride, rstride, a_hi, a_lo);
+                    build_mixed_part<L::C, L::R, L::S, MODE - 2, BF16>(kpart, xs, cstride, rstride, a_hi, a_lo);
                 } else if constexpr (FX != 0 && MODE == 1 && L::S % 2 == 1) {
                     const uint32_t xs_pair = xs - 4u * p.pf;  // 8-byte aligned (plan_ts)
                     build_pairs_part<L::C, L::R, L::S>(kpart, xs_pair, cstride, rstride, a_hi, a_lo);
                 } else if constexpr (FX != 0 && MODE == 0) {
-                    build_fixed_part<L::C, L::R, L::S>(kpart, xs, cstride, rstride, a_hi, a_lo, swap);
+                    build_fixed_part<L::C, L::R, L::S, BF16>(kpart, xs, cstride, rstride, a_hi, a_lo, swap);
                 }
             }
             for (int kc = kpart; kc < nchunks && FX == 0 && !(p.debug & 16); kc += KPARTS) {
@@ -528,12 +567,13 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                 wph ^= 1;
             }
             have = tw.t < p.total_tiles;
-            const uint32_t aph = ((i >> 1) & 1) ^ 1;
+            const int bn = p.nab == 2 ? (i & 1) : 0;  // the next tile's A buffer and its use count
+            const uint32_t aph = ((p.nab == 2 ? i >> 1 : i) & 1) ^ 1;
             bool s_ok = true, a_ok = true;
             if (have) {
                 xs = window_origin(tw, ws);
                 s_ok = ptx::mbar_test(&s_full[ws], wph);
-                a_ok = ptx::mbar_test(&a_empty[i & 1], aph);
+                a_ok = ptx::mbar_test(&a_empty[bn], aph);
             }
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
@@ -549,7 +589,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             if (have) {
                 if (!s_ok) ptx::mbar_wait(&s_full[ws], wph);
                 if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 1 : 11, i);
-                if (!a_ok) ptx::mbar_wait(&a_empty[i & 1], aph);
+                if (!a_ok) ptx::mbar_wait(&a_empty[bn], aph);
                 ptx::tc_fence_after();
             }
         }
@@ -628,7 +668,8 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     } else if (warp == TS_TMA_WARP) {
         // ============================ TMA: weights once, then input windows =============
         const uint32_t leader = ptx::elect_one();
-        const int wblocks = p.kb_w / 64;
+        constexpr int WBLK = BF16 ? 64 : 32;  // reduction elements per 128-byte weight row block
+        const int wblocks = p.kb_w / WBLK;
         // the weights are issued after the first window: the window heads the first tile's
         // chain (build -> MMA), the weights are first needed at the MMAs
         auto load_weights = [&]() {
@@ -639,11 +680,11 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                     uint8_t* dh = w_hi + (size_t)kb * p.w_rows * 128;
                     uint8_t* dl = w_lo + (size_t)kb * p.w_rows * 128;
                     if (CG == 2) {
-                        ptx::tma_load_2d_pair(dh, &tm_whi, ptx::leader_bar(w_full), kb * 64, row0);
-                        ptx::tma_load_2d_pair(dl, &tm_wlo, ptx::leader_bar(w_full), kb * 64, row0);
+                        ptx::tma_load_2d_pair(dh, &tm_whi, ptx::leader_bar(w_full), kb * WBLK, row0);
+                        ptx::tma_load_2d_pair(dl, &tm_wlo, ptx::leader_bar(w_full), kb * WBLK, row0);
                     } else {
-                        ptx::tma_load_2d(dh, &tm_whi, w_full, kb * 64, row0);
-                        ptx::tma_load_2d(dl, &tm_wlo, w_full, kb * 64, row0);
+                        ptx::tma_load_2d(dh, &tm_whi, w_full, kb * WBLK, row0);
+                        ptx::tma_load_2d(dl, &tm_wlo, w_full, kb * WBLK, row0);
                     }
                 }
             }
@@ -676,23 +717,25 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     } else {
         // ============================ MMA issuer ========================================
         const uint32_t leader = ptx::elect_one();
-        const uint32_t idesc = ptx::idesc_f32acc<true>(TS_BM * CG, p.n_pad);
+        const uint32_t idesc = ptx::idesc_f32acc<BF16>(TS_BM * CG, p.n_pad);
         const uint64_t dbh0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_hi));
         const uint64_t dbl0 = ptx::sdesc_k_sw128(ptx::smem_u32(w_lo));
         const uint32_t blk16 = (uint32_t)(p.w_rows * 128) >> 4;  // one 64-wide K block of B
-        const int ksteps = p.kp / 16;
+        const int ksteps = p.kp / (BF16 ? 16 : 8);  // one MMA covers 32 bytes of reduction per row
         if (rank == 0) ptx::mbar_wait(w_full, 0);
         int i = 0;
         for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles && rank == 0; tw.next(p), ++i) {
-            const int b = i & 1;
+            const int b = i & 1;  // accumulator
             const uint32_t ph = (i >> 1) & 1;
-            ptx::mbar_wait(&a_full[b], ph);
+            const int ba = p.nab == 2 ? b : 0;  // A buffer and the parity of its use count
+            const uint32_t pha = p.nab == 2 ? ph : (uint32_t)(i & 1);
+            ptx::mbar_wait(&a_full[ba], pha);
             if (leader) ts_stamp(p, 5, i);
             ptx::mbar_wait(&acc_empty[b], ph ^ 1);
             ptx::tc_fence_after();
             if (leader) ts_stamp(p, 6, i);
             const uint32_t d = tmem_base + b * p.n_pad;
-            const uint32_t a_hi = tmem_base + col_a0 + b * p.kp;
+            const uint32_t a_hi = tmem_base + col_a0 + ba * p.acols;
             const uint32_t a_lo = a_hi + half_cols;
             if (leader) {
                 for (int j = 0; j < ksteps && !(p.debug & 1); ++j) {
@@ -702,16 +745,16 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                         ptx::umma_ts_bf16_pair(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
                         ptx::umma_ts_bf16_pair(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
                     } else {
-                        ptx::umma_ts_bf16(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
-                        ptx::umma_ts_bf16(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
-                        ptx::umma_ts_bf16(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
+                        ptx::umma_ts<BF16>(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
+                        ptx::umma_ts<BF16>(d, a_hi + j * 8, dbl0 + boff, idesc, 1u);
+                        ptx::umma_ts<BF16>(d, a_hi + j * 8, dbh0 + boff, idesc, 1u);
                     }
                 }
                 if (CG == 2) {
-                    ptx::umma_commit_pair(&a_empty[b]);
+                    ptx::umma_commit_pair(&a_empty[ba]);
                     ptx::umma_commit_pair(&acc_full[b]);
                 } else {
-                    ptx::umma_commit(&a_empty[b]);
+                    ptx::umma_commit(&a_empty[ba]);
                     ptx::umma_commit(&acc_full[b]);
                 }
                 ts_stamp(p, 10, i);
@@ -739,6 +782,20 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
 // ----------------------------------------------------------------------------------------
 using TsKernel = void (*)(const TsParams, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                          const CUtensorMap);
+// the 3xTF32 kernels: compile-time layouts, single CTAs, plain or mixed reduction layout
+static TsKernel ts_kernel_tf32(int fixed, int mode) {
+    switch (fixed) {
+#define CB_TS_K(id, c, r, s)                                              \
+    case id:                                                              \
+        return mode == 3   ? conv_ts_kernel<1, id, 3, false>              \
+               : mode == 2 ? conv_ts_kernel<1, id, 2, false>              \
+                           : conv_ts_kernel<1, id, 0, false>;
+        CB_TS_FIXED_LIST(CB_TS_K)
+#undef CB_TS_K
+        default: return nullptr;
+    }
+}
+
 template <int CG>
 static TsKernel ts_kernel_for(int fixed, int mode) {
     switch (fixed) {
@@ -762,6 +819,8 @@ struct TsPlan {
     int nwin;
     bool tma_store;
     size_t smem;
+    bool bf16;
+    int nab, acols;  // A buffers in TMEM and the columns of one
 };
 
 static int ts_fixed_id(const Geom& g) {
@@ -773,9 +832,11 @@ static int ts_fixed_id(const Geom& g) {
     return 0;
 }
 
-static TsPlan plan_ts(const Geom& g) {
+static TsPlan plan_ts(const Geom& g, bool bf16 = true) {
     TsPlan pl{};
+    pl.bf16 = bf16;
     if (g.G != 1 || g.npix == 0) return pl;
+    if (!bf16 && !ts_fixed_id(g)) return pl;  // the tf32 split: compile-time layouts only
     // int32 tile walk and the float pixel -> row division (TileWalk, div_q)
     if (g.PQ >= (1 << 21) || (int64_t)g.N * ((g.PQ + TS_BM - 1) / TS_BM) >= (1LL << 31) - 1024) return pl;
     pl.n_pad = round_up(g.K, 16);
@@ -790,14 +851,19 @@ static TsPlan plan_ts(const Geom& g) {
         const char* e = env("CB_TS_PAIRMODE");
         return env("CB_TS_NO_PAIR") ? 0 : e ? std::atoi(e) : 2;
     }();
-    const int kd_pair = pair_mode == 2 ? mixed_kdim(g.C * g.R, g.S) : g.C * g.R * (g.S + 1);
-    if (pair_mode && ts_fixed_id(g) && g.S % 2 == 1 && g.sw % 2 == 0 &&
-        2 * pl.n_pad + 2 * round_up(kd_pair, 32) <= TS_TMEM_COLS)
-        pl.pair = pair_mode == 2 ? 2 : 1;
+    const int pm = (pair_mode == 1 && !bf16) ? 2 : pair_mode;  // no padded-pair tf32 kernels
+    const int kd_pair = pm == 2 ? mixed_kdim(g.C * g.R, g.S) : g.C * g.R * (g.S + 1);
+    // one A buffer holds hi and lo halves: kp / 2 + kp / 2 columns of bf16 pairs, kp + kp of tf32 words
+    const int per_el = bf16 ? 1 : 2;
+    if (pm && ts_fixed_id(g) && g.S % 2 == 1 && g.sw % 2 == 0 &&
+        2 * pl.n_pad + (bf16 ? 2 : 1) * per_el * round_up(kd_pair, 32) <= TS_TMEM_COLS)
+        pl.pair = pm == 2 ? 2 : 1;
     pl.kdim = pl.pair ? kd_pair : g.kdim;
     pl.kp = round_up(pl.kdim, 32);
     pl.kb_w = round_up(pl.kdim, 64);  // == cb_split_kdim(kdim)
-    if (pl.n_pad > 256 || 2 * pl.n_pad + 2 * pl.kp > TS_TMEM_COLS) return pl;
+    pl.acols = per_el * pl.kp;
+    pl.nab = 2 * pl.n_pad + 2 * pl.acols <= TS_TMEM_COLS ? 2 : 1;  // tf32 words: often one buffer only
+    if (pl.n_pad > 256 || 2 * pl.n_pad + pl.nab * pl.acols > TS_TMEM_COLS) return pl;
     // window columns: every tap of every output column (+ the pad tap past the last one)
     const int need = (g.Q - 1) * g.sw + (pl.x0 - g.pw) + (g.S - 1) * g.dw + 1 + (pl.pair == 1 && !pl.pf ? 1 : 0);
     pl.box_w = round_up(std::max(g.W + g.pw + pl.x0, need), 4);
@@ -812,9 +878,9 @@ static TsPlan plan_ts(const Geom& g) {
     {
         const char* e = env("CB_TS_CG");
         const int want = e ? std::atoi(e) : 1;  // pairs measured slower on cfg3 (30 vs 22 us)
-        if (want == 2 && pl.n_pad % 32 == 0 && pl.n_pad <= 256) pl.cg = 2;
+        if (want == 2 && bf16 && pl.n_pad % 32 == 0 && pl.n_pad <= 256) pl.cg = 2;
     }
-    pl.w_half_bytes = (uint32_t)(pl.n_pad / pl.cg) * pl.kb_w * 2;
+    pl.w_half_bytes = (uint32_t)(pl.n_pad / pl.cg) * pl.kb_w * (bf16 ? 2 : 4);
     // >= 120 KB keeps one CTA per SM (each allocates all 512 TMEM columns)
     pl.tma_store = (g.PQ % 4) == 0;  // 16-byte global strides for the output map
     auto smem_for = [&](int nwin) {
@@ -834,12 +900,12 @@ static TsPlan plan_ts(const Geom& g) {
 }
 
 // Used by fused_layout: the direct kernel serves this descriptor (bf16 split only).
-bool ts_eligible(const Geom& g) { return plan_ts(g).ok; }
+bool ts_eligible(const Geom& g, bool bf16) { return plan_ts(g, bf16).ok; }
 
 // The K7 weight layout: reduction length of the packed rows (C*R*(S+1) in pair mode) and,
 // in pair mode, the pad position (*pf = 1: pad tap first in each (c, r) row).
-int ts_weight_kdim(const Geom& g, int* pair, int* pf) {
-    const TsPlan pl = plan_ts(g);
+int ts_weight_kdim(const Geom& g, bool bf16, int* pair, int* pf) {
+    const TsPlan pl = plan_ts(g, bf16);
     *pair = pl.pair;
     *pf = pl.pf;
     return pl.pair ? pl.kdim : g.kdim;
@@ -848,8 +914,8 @@ int ts_weight_kdim(const Geom& g, int* pair, int* pf) {
 // The K7 reduction layout, element by element: map[k] = the OIHW index (c*R + r)*S + s of the
 // weight / window tap at reduction position k, or -1 for a zero element (pad taps, the tail).
 // Returns the layout's length (ts_weight_kdim), or -1 when K7 does not serve the descriptor.
-int ts_reduction_map(const Geom& g, int cap, int32_t* map) {
-    const TsPlan pl = plan_ts(g);
+int ts_reduction_map(const Geom& g, bool bf16, int cap, int32_t* map) {
+    const TsPlan pl = plan_ts(g, bf16);
     if (!pl.ok) return -1;
     const int kd = pl.pair ? pl.kdim : g.kdim;
     for (int k = 0; k < kd && k < cap; ++k) {
@@ -868,19 +934,19 @@ int ts_reduction_map(const Geom& g, int cap, int32_t* map) {
     return kd;
 }
 
-int ts_plan_query(const Geom& g, cb_tile_plan* out) {
-    const TsPlan pl = plan_ts(g);
+int ts_plan_query(const Geom& g, bool bf16, cb_tile_plan* out) {
+    const TsPlan pl = plan_ts(g, bf16);
     if (!pl.ok) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
     const int64_t tiles = (int64_t)g.N * ((g.PQ + TS_BM * pl.cg - 1) / (TS_BM * pl.cg));
-    out->variant = CB_VARIANT_TC3XBF16;
+    out->variant = bf16 ? CB_VARIANT_TC3XBF16 : CB_VARIANT_TC3XTF32;
     out->block_m = TS_BM * pl.cg;
     out->block_n = pl.n_pad;
-    out->block_k = 16;
-    out->stages = 2;
+    out->block_k = bf16 ? 16 : 8;
+    out->stages = pl.nab;
     out->splits = 1;
     out->m_tiles = tiles;
     out->n_tiles = 1;
-    out->k_blocks = pl.kp / 16;
+    out->k_blocks = pl.kp / (bf16 ? 16 : 8);
     out->ctas = (int)std::min<int64_t>(tiles, sm_count() / pl.cg) * pl.cg;
     return CB_OK;
 }
@@ -900,9 +966,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 ts_encode_fn() {
 
 unsigned long long* debug_trace_buffer(int ctas, cudaStream_t st);
 
-int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* w_lo,
+int launch_conv_ts(const Geom& g, bool bf16, const float* x, const void* w_hi, const void* w_lo,
                    const float* bias, float* y, cudaStream_t st) {
-    const TsPlan pl = plan_ts(g);
+    const TsPlan pl = plan_ts(g, bf16);
     if (!pl.ok) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv does not fit this descriptor");
     auto enc = ts_encode_fn();
     if (!enc) return fail(CB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -924,10 +990,10 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     }
     for (int h = 0; h < 2; ++h) {
         cuuint64_t dims[2] = {(cuuint64_t)pl.kb_w, (cuuint64_t)g.K};
-        cuuint64_t strides[1] = {(cuuint64_t)pl.kb_w * 2};
-        cuuint32_t box[2] = {64, (cuuint32_t)(pl.n_pad / pl.cg)};
+        cuuint64_t strides[1] = {(cuuint64_t)pl.kb_w * (bf16 ? 2 : 4)};
+        cuuint32_t box[2] = {bf16 ? 64u : 32u, (cuuint32_t)(pl.n_pad / pl.cg)};  // 128-byte rows
         cuuint32_t es[2] = {1, 1};
-        CUresult r = enc(h ? &mwl : &mwh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+        CUresult r = enc(h ? &mwl : &mwh, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                          const_cast<void*>(h ? w_lo : w_hi), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -968,12 +1034,16 @@ int launch_conv_ts(const Geom& g, const float* x, const void* w_hi, const void* 
     prm.stage_bytes = pl.stage_bytes;
     prm.stage_stride = pl.stage_stride;
     prm.nwin = pl.nwin;
+    prm.nab = pl.nab;
+    prm.acols = pl.acols;
     prm.w_half_bytes = pl.w_half_bytes;
     prm.w_rows = pl.n_pad / pl.cg;
     if (const char* dbg = env("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
     if (env("CB_TS_TRACE")) prm.trace = debug_trace_buffer(1024, st);
     const int mode = pl.pair == 2 ? 2 + pl.pf : pl.pair;
-    const TsKernel kern = pl.cg == 2 ? ts_kernel_for<2>(prm.fixed, mode) : ts_kernel_for<1>(prm.fixed, mode);
+    const TsKernel kern = !bf16 ? ts_kernel_tf32(prm.fixed, mode)
+                          : pl.cg == 2 ? ts_kernel_for<2>(prm.fixed, mode) : ts_kernel_for<1>(prm.fixed, mode);
+    if (!kern) return fail(CB_ERR_UNSUPPORTED, "direct TMEM conv: no tf32 kernel for this layout");
     {
         static std::mutex mu;
         static std::set<const void*> ready;  // kernels whose smem attribute is set

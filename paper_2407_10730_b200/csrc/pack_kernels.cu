@@ -412,9 +412,10 @@ int launch_weight_split(bool bf16, int rows, int kdim, int kdim_pad, const float
 
 // K3 for K7's pair layout: rows K x kdim_pad, k = (c*R + r)*(S+1) + s', the pad tap s' = 0
 // (pf = 1) or s' = S (pf = 0) zero, split into bf16 (hi, lo).
+template <bool BF16>
 __global__ void weight_split_pairs_kernel(int K, int C, int R, int S, int pf, int kdim_pad, int mixed,
-                                          const float* __restrict__ w, uint16_t* __restrict__ hi_out,
-                                          uint16_t* __restrict__ lo_out) {
+                                          const float* __restrict__ w, void* __restrict__ hi_out,
+                                          void* __restrict__ lo_out) {
     const int f = blockIdx.y;
     const int SP = S + 1, KD = C * R * SP;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kdim_pad; k += gridDim.x * blockDim.x) {
@@ -426,19 +427,27 @@ __global__ void weight_split_pairs_kernel(int K, int C, int R, int S, int pf, in
             const int cr = k / SP, s = k - cr * SP - pf;
             if (s >= 0 && s < S) v = w[((int64_t)f * C + cr / R) * R * S + (cr % R) * S + s];
         }
-        const uint16_t h = bf16_rn_bits(v);
-        hi_out[(int64_t)f * kdim_pad + k] = h;
-        lo_out[(int64_t)f * kdim_pad + k] = bf16_rn_bits(v - bf16_bits_to_f32(h));
+        if (BF16) {
+            const uint16_t h = bf16_rn_bits(v);
+            static_cast<uint16_t*>(hi_out)[(int64_t)f * kdim_pad + k] = h;
+            static_cast<uint16_t*>(lo_out)[(int64_t)f * kdim_pad + k] = bf16_rn_bits(v - bf16_bits_to_f32(h));
+        } else {
+            const Split2 sp = split_tf32(v);
+            static_cast<float*>(hi_out)[(int64_t)f * kdim_pad + k] = sp.hi;
+            static_cast<float*>(lo_out)[(int64_t)f * kdim_pad + k] = sp.lo;
+        }
     }
 }
 
-int launch_weight_split_pairs(const Geom& g, int pf, int kdim_pad, int mixed, const float* w, void* hi,
-                              void* lo, cudaStream_t st) {
+int launch_weight_split_pairs(const Geom& g, bool bf16, int pf, int kdim_pad, int mixed, const float* w,
+                              void* hi, void* lo, cudaStream_t st) {
     if (g.K == 0) return CB_OK;
     if (g.K > 65535) return fail(CB_ERR_UNSUPPORTED, "too many output channels for weight pack");
     const dim3 grid((unsigned)((kdim_pad + 255) / 256), (unsigned)g.K);
-    weight_split_pairs_kernel<<<grid, 256, 0, st>>>(g.K, g.C, g.R, g.S, pf, kdim_pad, mixed, w,
-                                                    static_cast<uint16_t*>(hi), static_cast<uint16_t*>(lo));
+    if (bf16)
+        weight_split_pairs_kernel<true><<<grid, 256, 0, st>>>(g.K, g.C, g.R, g.S, pf, kdim_pad, mixed, w, hi, lo);
+    else
+        weight_split_pairs_kernel<false><<<grid, 256, 0, st>>>(g.K, g.C, g.R, g.S, pf, kdim_pad, mixed, w, hi, lo);
     return check_launch("weight_split_pairs");
 }
 

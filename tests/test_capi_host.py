@@ -120,8 +120,13 @@ def test_workspace_and_layouts(lib):
     lay = algos.fused_layout(d, "tc3xbf16")
     assert lay["path"] == 1 and lay["chunk_bytes"] == 128 and lay["weight_cols"] == 2304
     assert lay["workspace_bytes"] >= 2 * 2 * 128 * 196 * 256  # NHWC hi + lo bf16
-    lay3 = algos.fused_layout(CONFIGS["cfg3"], "tc3xtf32")
-    assert lay3["path"] == 1 and lay3["chunk_bytes"] == 16  # C=3 padded to 4 channels
+    lay3 = algos.fused_layout(CONFIGS["cfg3"], "tc3xtf32")  # the direct kernel, tf32 words
+    assert lay3["path"] == 2 and lay3["workspace_bytes"] == 0 and lay3["weight_cols"] == 192
+    c8 = ConvDescriptor(batch=2, in_channels=8, in_h=32, in_w=32, out_channels=16, k_h=3, k_w=3,
+                        pad_h=1, pad_w=1)  # no compile-time layout: the tf32 split keeps K0 + K6
+    lay8 = algos.fused_layout(c8, "tc3xtf32")
+    assert lay8["path"] == 1 and lay8["chunk_bytes"] == 32  # 8 channels of 4-byte tf32 words
+    assert algos.fused_layout(c8, "tc3xbf16")["path"] == 2
     # depthwise with one channel per group cannot use 16-byte chunks: gather path
     dw = ConvDescriptor(batch=1, in_channels=8, in_h=9, in_w=9, out_channels=8, k_h=3, k_w=3,
                         groups=8)
@@ -229,3 +234,4 @@ def test_k7_reduction_map_is_a_permutation(lib, key, mixed):
                 assert b // S == a // S + 1 and b % S == a % S
     assert singles == (nr + 1) // 2
     assert algos.fused_layout(d, "tc3xbf16")["weight_cols"] == _capi.load().cb_split_kdim(len(m))
+    assert algos.fused_reduction_map(d, "tc3xtf32") == m  # the tf32 kernels use the same order

@@ -353,6 +353,28 @@ def test_direct_few_channel_conv(cuda, crs, stride, generic, monkeypatch):
         _check_conv(d, conv_fused(inp, variant="tc3xbf16"), orc.conv_direct_naive(d, x, w, b))
 
 
+@pytest.mark.parametrize("crs", [(3, 7, 7), (3, 3, 3), (3, 5, 5), (4, 3, 3), (4, 7, 7)])
+@pytest.mark.parametrize("stride", [1, 2])
+@pytest.mark.parametrize("layout", ["default", "plain"])
+def test_direct_few_channel_conv_tf32(cuda, crs, stride, layout, monkeypatch):
+    """K7 with the 3xTF32 split (tf32 words in TMEM, kind::tf32 MMAs, one or two A buffers):
+    every compile-time layout, the mixed and the plain reduction order, odd output sizes,
+    bias, batch > 1, many tiles per CTA."""
+    from paper_2407_10730_b200.algos import conv_fused, fused_layout
+    from paper_2407_10730_b200.descriptor import ConvDescriptor
+    c, r, s = crs
+    if layout == "plain":
+        monkeypatch.setenv("CB_TS_NO_PAIR", "1")
+    for d in (ConvDescriptor(batch=2, in_channels=c, in_h=37, in_w=44, out_channels=24, k_h=r, k_w=s,
+                             stride_h=stride, stride_w=stride, pad_h=r // 2, pad_w=s // 2, has_bias=True),
+              ConvDescriptor(batch=3, in_channels=c, in_h=160, in_w=192,
+                             out_channels=64 if c * r * s <= 100 else 32, k_h=r, k_w=s,
+                             stride_h=2, stride_w=stride, pad_h=r // 2, pad_w=s // 2)):
+        assert fused_layout(d, "tc3xtf32")["path"] == 2, d
+        inp, (x, w, b) = _inputs(d)
+        _check_conv(d, conv_fused(inp, variant="tc3xtf32"), orc.conv_direct_naive(d, x, w, b))
+
+
 def test_direct_few_channel_conv_is_repeatable(cuda):
     """K7's pipeline (window ring, TMEM A ring, two accumulators, cross-tile barrier tests)
     gives bit-identical results launch after launch on a grid with many tiles per CTA."""
