@@ -56,6 +56,8 @@ struct TsParams {
                         // kp for tf32 words)
     int nab;            // A buffers in TMEM: 2, or 1 when only one fits (tf32)
     int acols;          // TMEM columns of one A buffer (hi + lo halves)
+    int khalves;        // 2: the single tf32 A buffer is used as two half-K buffers (a ring over
+                        // (tile, K half): the build of one half overlaps the MMAs of the other)
     int n_pad;          // output channels padded to 16 (MMA N)
     int kb_w;           // split weight row length (multiple of 64)
     int tiles_per_img;  // ceil(PQ / (128 * CG)): tiles of one CTA (CG = 1) or pair (CG = 2)
@@ -162,9 +164,13 @@ __device__ __forceinline__ void split_store_group(const float (&u)[8], uint32_t 
         uint32_t hv[8], lv[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const Split2 sp = split_tf32(u[e]);
-            hv[e] = __float_as_uint(sp.hi);
-            lv[e] = __float_as_uint(sp.lo);
+            // kind::tf32 reads the top 19 bits of an operand word, so the hi half is the
+            // value itself and lo = v - trunc_tf32(v) is exact (<= 13 significant bits, read
+            // to 11: 2^-21 |v|, below the dropped lo * lo term).  No cvt.rna.tf32 -- those
+            // conversions made the tf32 build 2.7x the bf16 one (2680 vs 980 cycles a tile).
+            const uint32_t bits = __float_as_uint(u[e]);
+            hv[e] = bits;
+            lv[e] = __float_as_uint(u[e] - __uint_as_float(bits & 0xffffe000u));
         }
         ptx::tmem_st_32x32b_groups(a_hi + g * 8, hv, 2);
         ptx::tmem_st_32x32b_groups(a_lo + g * 8, lv, 2);
@@ -418,7 +424,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
     const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;
     const int unit0 = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;
     const int col_a0 = 2 * p.n_pad;  // TMEM: [acc0 | acc1 | A0 (hi, lo) | A1 (hi, lo)]
-    const int half_cols = BF16 ? p.kp / 2 : p.kp;
+    const int half_cols = (BF16 || p.khalves == 2) ? p.kp / 2 : p.kp;
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(w_full, 1);
@@ -512,11 +518,52 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             ptx::tc_fence_after();
         }
         while (have) {
-            const int b = p.nab == 2 ? (i & 1) : 0;  // A buffer of tile i
+            const bool halves = !BF16 && FX != 0 && KPARTS == 1 && p.khalves == 2;
+            const int b = p.nab == 2 ? (i & 1) : halves ? 1 : 0;  // A buffer this iteration hands over last
             if (lane == 0 && (warp == 0 || warp == 8)) ts_stamp(p, warp == 0 ? 2 : 12, i);
             const uint32_t a_hi = lane_addr + col_a0 + b * p.acols;
             const uint32_t a_lo = a_hi + half_cols;
-            if (FX != 0 && !(p.debug & 16)) {
+            if constexpr (!BF16 && FX != 0 && KPARTS == 1) {
+                if (halves) {
+                    const bool build = !(p.debug & 16);
+                    // K halves: groups [0, GH) go to buffer 0 and are handed to the MMA warp,
+                    // then groups [GH, G) to buffer 1 (each buffer kp columns: hi | lo)
+                    using L = TsLayout<FX>;
+                    constexpr int KD = MODE >= 2 ? mixed_kdim(L::C * L::R, L::S) : L::C * L::R * L::S;
+                    constexpr int KP = (KD + 31) / 32 * 32, G = (KD + 7) / 8, GH = KP / 16;
+                    static_assert(G > GH, "the second K half holds at least one group");
+                    const uint32_t cstride = 4u * p.box_rows * p.box_w, rstride = 4u * g.dh * p.box_w;
+                    const uint32_t base0 = lane_addr + col_a0, base1 = base0 + KP;
+                    if (build) {
+                        if constexpr (MODE >= 2)
+                            build_mixed<L::C, L::R, L::S, MODE - 2, 0, GH, false>(xs, cstride, rstride, base0, base0 + KP / 2);
+                        else
+                            build_fixed<L::C, L::R, L::S, 0, GH, false>(xs, cstride, rstride, base0, base0 + KP / 2, swap);
+                    }
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&a_full[0]);
+                    ptx::mbar_wait(&a_empty[1], (uint32_t)(i & 1) ^ 1);
+                    ptx::tc_fence_after();
+                    if (i == 0 && build) {  // columns past the written groups of the second half: zero once
+                        const uint32_t z[4] = {0u, 0u, 0u, 0u};
+                        for (int c4 = (G - GH) * 8; c4 < KP / 2; c4 += 4) {
+                            ptx::tmem_st_32x32b_x4(base1 + c4, z);
+                            ptx::tmem_st_32x32b_x4(base1 + KP / 2 + c4, z);
+                        }
+                    }
+                    if (build) {
+                        if constexpr (MODE >= 2)
+                            build_mixed<L::C, L::R, L::S, MODE - 2, GH, G, false>(xs, cstride, rstride, base1 - GH * 8,
+                                                                                  base1 + KP / 2 - GH * 8);
+                        else
+                            build_fixed<L::C, L::R, L::S, GH, G, false>(xs, cstride, rstride, base1 - GH * 8,
+                                                                        base1 + KP / 2 - GH * 8, swap);
+                    }
+                }
+            }
+            if (FX != 0 && !(p.debug & 16) && !halves) {
                 if (i < p.nab) {  // columns past the written groups: zero once per A buffer
                     const uint32_t z[4] = {0u, 0u, 0u, 0u};
                     const int kd = MODE == 1 ? g.C * g.R * (g.S + 1) : MODE >= 2 ? mixed_kdim(g.C * g.R, g.S) : g.kdim;
@@ -727,6 +774,32 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
         for (TileWalk tw(p, unit0, nunits); tw.t < p.total_tiles && rank == 0; tw.next(p), ++i) {
             const int b = i & 1;  // accumulator
             const uint32_t ph = (i >> 1) & 1;
+            if (!BF16 && p.khalves == 2) {  // two K halves per tile through the two A buffers
+                ptx::mbar_wait(&acc_empty[b], ph ^ 1);
+                const uint32_t d = tmem_base + b * p.n_pad;
+                for (int h = 0; h < 2; ++h) {
+                    ptx::mbar_wait(&a_full[h], (uint32_t)(i & 1));
+                    ptx::tc_fence_after();
+                    if (leader) ts_stamp(p, h ? 6 : 5, i);
+                    const uint32_t a_hi = tmem_base + col_a0 + h * p.kp, a_lo = a_hi + p.kp / 2;
+                    if (leader) {
+                        for (int jj = 0; jj < ksteps / 2 && !(p.debug & 1); ++jj) {
+                            const int j = h * (ksteps / 2) + jj;
+                            const uint64_t boff = (uint64_t)((j >> 2) * blk16 + (j & 3) * 2);
+                            ptx::umma_ts<BF16>(d, a_lo + jj * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
+                            ptx::umma_ts<BF16>(d, a_hi + jj * 8, dbl0 + boff, idesc, 1u);
+                            ptx::umma_ts<BF16>(d, a_hi + jj * 8, dbh0 + boff, idesc, 1u);
+                        }
+                        ptx::umma_commit(&a_empty[h]);
+                        if (h == 1) {
+                            ptx::umma_commit(&acc_full[b]);
+                            ts_stamp(p, 10, i);
+                        }
+                    }
+                    __syncwarp();
+                }
+                continue;
+            }
             const int ba = p.nab == 2 ? b : 0;  // A buffer and the parity of its use count
             const uint32_t pha = p.nab == 2 ? ph : (uint32_t)(i & 1);
             ptx::mbar_wait(&a_full[ba], pha);
@@ -821,6 +894,7 @@ struct TsPlan {
     size_t smem;
     bool bf16;
     int nab, acols;  // A buffers in TMEM and the columns of one
+    int khalves;     // 2: the single tf32 buffer split into two half-K buffers
 };
 
 static int ts_fixed_id(const Geom& g) {
@@ -864,6 +938,7 @@ static TsPlan plan_ts(const Geom& g, bool bf16 = true) {
     pl.acols = per_el * pl.kp;
     pl.nab = 2 * pl.n_pad + 2 * pl.acols <= TS_TMEM_COLS ? 2 : 1;  // tf32 words: often one buffer only
     if (pl.n_pad > 256 || 2 * pl.n_pad + pl.nab * pl.acols > TS_TMEM_COLS) return pl;
+    pl.khalves = (!bf16 && pl.nab == 1 && CB_TS_KPARTS == 1 && !env("CB_TS_NO_HALVES")) ? 2 : 1;
     // window columns: every tap of every output column (+ the pad tap past the last one)
     const int need = (g.Q - 1) * g.sw + (pl.x0 - g.pw) + (g.S - 1) * g.dw + 1 + (pl.pair == 1 && !pl.pf ? 1 : 0);
     pl.box_w = round_up(std::max(g.W + g.pw + pl.x0, need), 4);
@@ -1036,6 +1111,7 @@ int launch_conv_ts(const Geom& g, bool bf16, const float* x, const void* w_hi, c
     prm.nwin = pl.nwin;
     prm.nab = pl.nab;
     prm.acols = pl.acols;
+    prm.khalves = pl.khalves;
     prm.w_half_bytes = pl.w_half_bytes;
     prm.w_rows = pl.n_pad / pl.cg;
     if (const char* dbg = env("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
