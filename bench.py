@@ -759,6 +759,15 @@ def run_ours(args, ranks):
                                          for c, r in table.items()
                                          if r["fused"].get("kernel_alone_roofline_frac")},
             "fused_60pct_met": {c: r["fused"]["target_60pct_met"] for c, r in table.items()},
+            # the same for the north star's own split (3xTF32), where it is not the default
+            "fused_conv_roofline_frac_3xtf32": {
+                c: round(r[k]["kernel_alone_roofline_frac"], 3) for c, r in table.items()
+                for k in (("fused_tf32",) if "fused_tf32" in r else ("fused",))
+                if r[k]["variant"] == "tc3xtf32" and r[k].get("kernel_alone_roofline_frac")},
+            "fused_60pct_met_3xtf32": {
+                c: r[k]["target_60pct_met"] for c, r in table.items()
+                for k in (("fused_tf32",) if "fused_tf32" in r else ("fused",))
+                if r[k]["variant"] == "tc3xtf32"},
             "pack_hbm_frac": {c: {"K1_im2col": round(r["im2col_gemm"]["pack_alone_hbm_frac"], 3),
                                   "K2_slices": round(r["sconv"]["pack_alone_hbm_frac"], 3)}
                               for c, r in table.items()
