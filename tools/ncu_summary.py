@@ -67,6 +67,10 @@ def raw_metrics(rep: Path) -> list[dict]:
 
 def short_name(kernel: str) -> str:
     base = kernel.replace("void ", "").split("(")[0].split("<")[0].split("::")[-1]
+    if base == "conv_ts_kernel":  # the last template argument: 1 / true = bf16 pairs, 0 / false = tf32 words
+        args = kernel.split("(")[0].split("<")[-1].split(">")[0].replace(" ", "").replace("(bool)", "").split(",")
+        if len(args) >= 4 and args[-1] in ("0", "false"):
+            return "conv_ts_tf32"
     return SHORT.get(base, base)
 
 
