@@ -18,6 +18,11 @@
 //     tcgen05.mma kind::f16 with A read from TMEM and B (weights, K-major SW128) from smem;
 //   * four epilogue warps drain the double-buffered TMEM accumulator into NCHW (+bias).
 //
+// The 3xTF32 split (compile-time layouts) keeps tf32 words in TMEM instead of bf16 pairs --
+// hi is the value itself, lo = v - trunc_tf32(v), no conversions -- and issues kind::tf32
+// MMAs of 8 reduction elements; when only one whole-K A buffer fits, it is used as two
+// half-K buffers so the build of one half overlaps the MMAs of the other.
+//
 // Tiles are 128 consecutive output pixels of one image; the persistent grid walks them.
 // HBM traffic is the algorithmic minimum: x read once (the window re-reads hit L2), y
 // written once, the weights once per CTA.
@@ -857,6 +862,7 @@ using TsKernel = void (*)(const TsParams, const CUtensorMap, const CUtensorMap, 
                          const CUtensorMap);
 // the 3xTF32 kernels: compile-time layouts, single CTAs, plain or mixed reduction layout
 static TsKernel ts_kernel_tf32(int fixed, int mode) {
+    if (mode == 1) return nullptr;  // no padded-pair tf32 kernels (plan_ts never asks for one)
     switch (fixed) {
 #define CB_TS_K(id, c, r, s)                                              \
     case id:                                                              \
