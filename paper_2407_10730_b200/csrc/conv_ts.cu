@@ -61,6 +61,7 @@ struct TsParams {
                         // kp for tf32 words)
     int nab;            // A buffers in TMEM: 2, or 1 when only one fits (tf32)
     int acols;          // TMEM columns of one A buffer (hi + lo halves)
+    int ksteps_real;    // MMA K steps that hold reduction elements (the rest of kp is zero padding)
     int khalves;        // 2: the single tf32 A buffer is used as two half-K buffers (a ring over
                         // (tile, K half): the build of one half overlaps the MMAs of the other)
     int n_pad;          // output channels padded to 16 (MMA N)
@@ -790,6 +791,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
                     if (leader) {
                         for (int jj = 0; jj < ksteps / 2 && !(p.debug & 1); ++jj) {
                             const int j = h * (ksteps / 2) + jj;
+                            if (j >= p.ksteps_real) break;  // all-zero padding steps
                             const uint64_t boff = (uint64_t)((j >> 2) * blk16 + (j & 3) * 2);
                             ptx::umma_ts<BF16>(d, a_lo + jj * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
                             ptx::umma_ts<BF16>(d, a_hi + jj * 8, dbl0 + boff, idesc, 1u);
@@ -816,7 +818,7 @@ conv_ts_kernel(const __grid_constant__ TsParams p, const __grid_constant__ CUten
             const uint32_t a_hi = tmem_base + col_a0 + ba * p.acols;
             const uint32_t a_lo = a_hi + half_cols;
             if (leader) {
-                for (int j = 0; j < ksteps && !(p.debug & 1); ++j) {
+                for (int j = 0; j < min(ksteps, p.ksteps_real) && !(p.debug & 1); ++j) {
                     const uint64_t boff = (uint64_t)((j >> 2) * blk16 + (j & 3) * 2);
                     if (CG == 2) {
                         ptx::umma_ts_bf16_pair(d, a_lo + j * 8, dbh0 + boff, idesc, j > 0 ? 1u : 0u);
@@ -1118,6 +1120,7 @@ int launch_conv_ts(const Geom& g, bool bf16, const float* x, const void* w_hi, c
     prm.nab = pl.nab;
     prm.acols = pl.acols;
     prm.khalves = pl.khalves;
+    prm.ksteps_real = env("CB_TS_ALL_KSTEPS") ? pl.kp : (pl.kdim + (bf16 ? 15 : 7)) / (bf16 ? 16 : 8);
     prm.w_half_bytes = pl.w_half_bytes;
     prm.w_rows = pl.n_pad / pl.cg;
     if (const char* dbg = env("CB_TS_DEBUG")) prm.debug = std::atoi(dbg);
